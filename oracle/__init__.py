@@ -1,0 +1,125 @@
+"""oracle/ — TEST INFRASTRUCTURE ONLY (never imported by the product path).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package.  It shares no code with
+paper_1404_4152_b200/ and neither imports the other; both read inputs from
+swdata/ only.
+
+* `sw_score`, `scores`: Eq. 1 as printed, scalar int32,
+  linear space (sw_oracle.c), threaded over subjects for whole databases.
+* `sw_full`: Gotoh full matrix with -inf boundaries (pins reading R2).
+* `topk`: stage (iv) "sort all alignment scores in descending order"
+   by a full sort, tie-break id ascending (reading R7).
+* `brute.brute_force`: enumeration of every local alignment (tiny inputs).
+
+Pinned by tests/test_oracle.py (-m "not gpu"); no function is parity-unpinned.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "_liboracle.so")
+_SRC = os.path.join(_HERE, "sw_oracle.c")
+_lib = None
+
+CFLAGS = ["-O2", "-shared", "-fPIC", "-pthread"]
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _SO, _SRC])
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        i32, i64 = ctypes.c_int32, ctypes.c_int64
+        L.oracle_sw_score.argtypes = [P, i32, P, i32, P, i32, i32]
+        L.oracle_sw_score.restype = i32
+        L.oracle_sw_full.argtypes = [P, i32, P, i32, P, i32, i32]
+        L.oracle_sw_full.restype = i32
+        L.oracle_scores.argtypes = [P, i32, P, P, P, i64, P, i32, i32, ctypes.c_int, P]
+        L.oracle_scores.restype = ctypes.c_int
+        L.oracle_topk.argtypes = [P, P, i64, i32, P, P]
+        L.oracle_topk.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _u8(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint8))
+
+
+def _m32(M):
+    M = np.asarray(M)
+    if M.shape != (32, 32):
+        out = np.zeros((32, 32), dtype=np.int8)
+        out[:M.shape[0], :M.shape[1]] = M
+        M = out
+    return np.ascontiguousarray(M, dtype=np.int8)
+
+
+def sw_score(q, s, M, alpha: int, beta: int) -> int:
+    q, s, M = _u8(q), _u8(s), _m32(M)
+    r = lib().oracle_sw_score(q.ctypes.data, q.size, s.ctypes.data, s.size, M.ctypes.data, alpha, beta)
+    if r < 0:
+        raise MemoryError("oracle_sw_score")
+    return int(r)
+
+
+def sw_full(q, s, M, alpha: int, beta: int) -> int:
+    q, s, M = _u8(q), _u8(s), _m32(M)
+    r = lib().oracle_sw_full(q.ctypes.data, q.size, s.ctypes.data, s.size, M.ctypes.data, alpha, beta)
+    if r < 0:
+        raise MemoryError("oracle_sw_full")
+    return int(r)
+
+
+def default_threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def scores(query, residues, offsets, lengths, M, alpha: int, beta: int, nthreads: int | None = None) -> np.ndarray:
+    """Eq. 1 score of `query` against every subject (input order), int32."""
+    q, res, M = _u8(query), _u8(residues), _m32(M)
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    lens = np.ascontiguousarray(lengths, dtype=np.int32)
+    out = np.empty(lens.size, dtype=np.int32)
+    rc = lib().oracle_scores(q.ctypes.data, q.size, res.ctypes.data if res.size else None,
+                             offs.ctypes.data, lens.ctypes.data, lens.size, M.ctypes.data,
+                             alpha, beta, nthreads or default_threads(), out.ctypes.data)
+    if rc != 0:
+        raise MemoryError("oracle_scores")
+    return out
+
+
+def db_scores(query, db, M, alpha, beta, nthreads=None, sample=None):
+    """`scores` over a swdata.SynthDB, optionally on the index subset `sample`."""
+    if sample is None:
+        return scores(query, db.residues, db.offsets, db.lengths, M, alpha, beta, nthreads)
+    sample = np.asarray(sample, dtype=np.int64)
+    return scores(query, db.residues, db.offsets[sample], db.lengths[sample], M, alpha, beta, nthreads)
+
+
+def topk(scores_, k: int, ids=None):
+    """(ids int64[k], scores int32[k]) by (score desc, id asc); (-1,-1) past n."""
+    sc = np.ascontiguousarray(scores_, dtype=np.int32)
+    idp = None
+    if ids is not None:
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        idp = ids.ctypes.data
+    oi = np.empty(k, dtype=np.int64)
+    os_ = np.empty(k, dtype=np.int32)
+    if lib().oracle_topk(sc.ctypes.data, idp, sc.size, k, oi.ctypes.data, os_.ctypes.data) != 0:
+        raise MemoryError("oracle_topk")
+    return oi, os_
