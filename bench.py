@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py — GCUPS of one-query Smith-Waterman database search on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C2] [--first-stage 16]
+
+A step is one pass of the whole hot path (query profile,
+inter-task int16x2 pass, int32 rerun of saturated subjects, scatter + exact
+top-k) over the workload of BASELINE.json configs[1] (C2: one query of length
+464 vs 1M synthetic sequences, BLOSUM62, alpha=2, beta=12, top-10).  With
+N > 1 (torchrun, one rank per GPU) every rank holds a 1M-sequence shard of an
+N x 1M database (weak scaling), partitioned by residue count (snake order over
+the length-sorted ids), and the per-rank top-k lists are merged through an
+NCCL all_gather inside the timed step.
+
+`value` is device time with the database and query resident; `e2e` is the same
+metric through the blocking C-ABI call sw_search with host buffers (query and
+matrix H2D, all scores + top-k D2H inside the timed region).
+--impl reference times the CPU oracle (oracle/, the correctness reference) on a
+bounded sample of the same workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GCUPS (query x db cells/s) at 1/2/4/8 B200; fraction of DPX/int roofline"
+SMS = 148
+ALU_LANES_PER_CLK = 64      # measured: VIADDMNMX/VIMNMX3 .S16x2 thread-ops/clk/SM (profiles/r01_dpx_microbench.txt)
+ALU_OPS_PER_CELL = 1.75     # minimal Eq. 1 update in int16x2: (VIMNMX3 + 2 VIADDMNMX.RELU + 1/2 VIMNMX3) / 2 cells
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def snake_partition(lengths: np.ndarray, world: int, rank: int) -> np.ndarray:
+    """Ids of rank's shard: global stable sort by (length, id), sorted rank r goes
+    to GPU r mod 2P if < P else 2P-1-(r mod 2P); ascending ids."""
+    from paper_1404_4152_b200.dist import snake_shard
+    return snake_shard(lengths, world, rank)
+
+
+def build_workload(cfg_name: str, world: int, rank: int, n_per_rank: int | None):
+    from swdata import CONFIGS, make_db, make_query
+    from swdata.synth import Config, db_lengths
+    base = CONFIGS[cfg_name]
+    n_total = (n_per_rank or base.n_seqs) * world
+    cfg = Config(**{**base.__dict__, "n_seqs": n_total}) if n_total != base.n_seqs else base
+    lengths_kind = db_lengths(cfg)
+    ids = snake_partition(lengths_kind[0], world, rank) if world > 1 else None
+    db = make_db(cfg, ids=ids, lengths_kind=lengths_kind)
+    q = make_query(base)
+    return base, cfg, db, q, int(lengths_kind[0].sum())
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (as it stands) on a bounded sample."""
+    if rank != 0:
+        return
+    import oracle
+    from swdata import CONFIGS, make_db, make_query
+    base = CONFIGS[args.config]
+    q = make_query(base)
+    M = base.matrix32()
+    cores = oracle.default_threads()
+    rng = np.random.default_rng(0)
+    n_sample = args.ref_sample
+    steps = []
+    full = make_db(base)
+    cells_per_step = []
+    for s in range(args.warmup + args.steps):
+        idx = np.sort(rng.choice(full.n_seqs, size=n_sample, replace=False))
+        t0 = time.perf_counter()
+        oracle.db_scores(q, full, M, base.alpha, base.beta, nthreads=cores, sample=idx)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            steps.append(dt)
+            cells_per_step.append(int(full.lengths[idx].sum()) * q.size)
+    tot = sum(steps)
+    gcups = sum(cells_per_step) / tot / 1e9
+    line = {"metric": METRIC, "value": round(gcups, 4), "unit": "GCUPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{base.name}: query {q.size} vs {base.n_seqs} synthetic seqs "
+                                   f"(lognormal mean 350), BLOSUM62 2/12; each step a random sample of "
+                                   f"{n_sample} subjects", "k": base.k},
+            "cpu_baseline": {"value": round(gcups, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
+                             "sample": f"{n_sample} random subjects of {base.name} per step"},
+            "e2e": {"value": round(gcups, 4), "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(base, q, db, seconds_target=12.0):
+    """Oracle timed on this host's cores on a bounded random sample of the workload."""
+    import oracle
+    cores = oracle.default_threads()
+    M = base.matrix32()
+    rng = np.random.default_rng(1)
+    # calibrate on a small sample, then size the sample for ~seconds_target
+    idx = np.sort(rng.choice(db.n_seqs, size=min(2000, db.n_seqs), replace=False))
+    t0 = time.perf_counter()
+    oracle.db_scores(q, db, M, base.alpha, base.beta, nthreads=cores, sample=idx)
+    dt = max(time.perf_counter() - t0, 1e-3)
+    n = int(min(db.n_seqs, max(2000, idx.size * seconds_target / dt)))
+    idx = np.sort(rng.choice(db.n_seqs, size=n, replace=False))
+    t0 = time.perf_counter()
+    oracle.db_scores(q, db, M, base.alpha, base.beta, nthreads=cores, sample=idx)
+    dt = time.perf_counter() - t0
+    cells = int(db.lengths[idx].sum()) * q.size
+    return {"value": round(cells / dt / 1e9, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
+            "sample": f"{n} random subjects of the rank-0 shard ({cells:.3e} cells, {dt:.1f} s)"}
+
+
+def load_ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_inter16_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--first-stage", type=int, default=16)
+    ap.add_argument("--n-per-rank", type=int, default=None)
+    ap.add_argument("--ref-sample", type=int, default=20000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1404_4152_b200 as sw
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    base, cfg, sdb, q, total_res = build_workload(args.config, world, rank, args.n_per_rank)
+    M = base.matrix32()
+    k = base.k
+    t_create = time.perf_counter()
+    db = sw.Database.from_synth(sdb, global_ids=sdb.global_ids if world > 1 else None, device=local,
+                                first_stage=args.first_stage)
+    t_create = time.perf_counter() - t_create
+    n = sdb.n_seqs
+    cells_local = int(sdb.lengths.sum()) * q.size
+    cells_total = total_res * q.size
+
+    stream = torch.cuda.Stream()
+    d_scores = torch.empty(n, dtype=torch.int32, device="cuda")
+    d_ti = torch.empty(k, dtype=torch.int64, device="cuda")
+    d_ts = torch.empty(k, dtype=torch.int32, device="cuda")
+    g_ti = torch.empty(world * k, dtype=torch.int64, device="cuda")
+    g_ts = torch.empty(world * k, dtype=torch.int32, device="cuda")
+
+    def step():
+        db.search_async(q, M, base.alpha, base.beta, k, d_scores, d_ti, d_ts, stream=stream)
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.all_gather_into_tensor(g_ti, d_ti)
+                dist.all_gather_into_tensor(g_ts, d_ts)
+
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    info0 = db.info()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        dist.barrier()
+    info1 = db.info()
+    launches = info1["launches"] - info0["launches"]
+    stage = [db.stage_times(b) for b in range(1, min(args.steps, 64) + 1)]
+    ms_inter = statistics.mean(s[1] for s in stage)
+    ms_rerun = statistics.mean(s[2] for s in stage)
+    ms_step = ms_total / args.steps
+    gcups = cells_total / (ms_step * 1e-3) / 1e9
+
+    # merged top-k (host merge of the gathered lists; checked once, outside timing)
+    if world > 1:
+        mi, ms = sw.merge_topk(g_ti.view(world, k).cpu().numpy(), g_ts.view(world, k).cpu().numpy(), k)
+    else:
+        mi, ms = d_ti.cpu().numpy(), d_ts.cpu().numpy()
+
+    # ---- e2e: blocking C-ABI call with host buffers (H2D query+matrix, D2H scores + top-k) ----
+    e2e = None
+    if not args.no_e2e:
+        h_scores = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+        h_ti = torch.empty(k, dtype=torch.int64, pin_memory=True).numpy()
+        h_ts = torch.empty(k, dtype=torch.int32, pin_memory=True).numpy()
+        for _ in range(2):
+            db.search(q, M, base.alpha, base.beta, k, scores=h_scores, topk_ids=h_ti, topk_scores=h_ts)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            db.search(q, M, base.alpha, base.beta, k, scores=h_scores, topk_ids=h_ti, topk_scores=h_ts)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": round(cells_total / (dt / args.steps) / 1e9, 2), "unit": "GCUPS",
+               "h2d_bytes_per_step": int(q.size + 1024), "d2h_bytes_per_step": int(4 * n + 12 * k),
+               "api": "sw_search (blocking, pinned host buffers)"}
+
+    if rank == 0:
+        f_run = (clk.get("sm_mhz") or 1965.0) * 1e6
+        peak_max = SMS * 1965e6 * ALU_LANES_PER_CLK / ALU_OPS_PER_CELL / 1e9
+        peak_run = SMS * f_run * ALU_LANES_PER_CLK / ALU_OPS_PER_CELL / 1e9
+        achieved = cells_local / (ms_inter * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": round(gcups, 2), "unit": "GCUPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int16x2+int32",
+            "data": "synthetic",
+            "config": {"workload": f"{base.name} (BASELINE.json configs[1]): query {q.size} vs "
+                                   f"{n} synthetic seqs per GPU (lognormal mean 350, [10,5000]), "
+                                   f"BLOSUM62 alpha=2 beta=12, all scores + top-{k}",
+                       "seqs_total": cfg.n_seqs, "residues_total": total_res, "cells_per_step": cells_total,
+                       "k": k, "first_stage": args.first_stage,
+                       "l2": "inputs larger than L2 (packed DB %.0f MB/GPU > 126 MB)" % (info1["packed_bytes"] / 1e6),
+                       "parallelism": f"dp{world} (residue-balanced shards)" if world > 1 else "1 GPU"},
+            "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_max, 1),
+                         "unit": "Gcell/s", "frac": round(achieved / peak_max, 4),
+                         "frac_at_run_clock": round(achieved / peak_run, 4),
+                         "kernel": "k_inter16 (int16x2 DPX first pass)",
+                         "kernel_ms": round(ms_inter, 4), "kernel_share_of_step": round(ms_inter / ms_step, 4),
+                         "peak_basis": "148 SM x 1965 MHz x 64 DPX lanes/clk/SM (measured) / 1.75 alu-pipe ops per cell",
+                         "traffic": load_ncu_traffic()},
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "rerun_ms": round(ms_rerun, 4),
+            "db_create_s": round(t_create, 2),
+            "topk_head": [int(x) for x in ms[:3]],
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(base, q, sdb)
+        elif not args.no_cpu_baseline:
+            line["cpu_baseline"] = None
+        print(json.dumps(line), flush=True)
+    db.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * swsearch.h — C ABI of the B200-native Smith-Waterman protein database search.
+ *
+ * What is computed (§II.A, Eq. 1): for a query S1 = q[1..m]
+ * and every database subject S2 = s[1..n], the optimal local alignment score
+ *
+ *   H(i,j) = max{ 0, H(i-1,j-1) + fsbt(S1[i],S2[j]), E(i,j), F(i,j) }
+ *   E(i,j) = max{ E(i-1,j) - alpha, H(i-1,j) - beta }
+ *   F(i,j) = max{ F(i,j-1) - alpha, H(i,j-1) - beta }
+ *   H(i,0) = H(0,j) = E(0,j) = F(i,0) = 0,   score = max over H,
+ *
+ * "alpha is the gap extension penalty, beta is the sum of gap open and
+ * extension penalties"; the paper's "10-2k" is alpha=2, beta=12
+ * (PAPER.md:164).  Results are exact int32 (32-bit lanes): the
+ * device computes in packed int16x2 and reruns in int32 every subject whose
+ * 16-bit pass could have saturated (DESIGN.md §"Saturation").
+ *
+ * The workflow follows the paper's four stages (§III, Fig. 2):
+ * sw_db_create = the offline index (subjects sorted by length); sw_search =
+ * (i) query profile, (ii) alignment on the device, (iii) wait, (iv) rank all
+ * scores in descending order (here: exact top-k, ties by ascending id).
+ *
+ * Conventions (DESIGN.md §"Readings"):
+ *  - residue codes: 0..23 = "ARNDCQEGHILKMFPSTWYVBZX*"; code 24 (DUMMY) is
+ *    internal padding scoring 0 against everything.  Inputs with
+ *    a code >= 24 are rejected (SW_EINVAL).
+ *  - matrix: 32x32 int8, row-major, row = QUERY residue, column = SUBJECT
+ *    residue: fsbt(S1[i], S2[j]) = matrix[32*q_i + s_j].  Rows and columns
+ *    24..31 must be 0 (SW_EINVAL otherwise).
+ *  - 0 <= alpha <= beta <= 32767 (SW_EINVAL otherwise); qlen >= 1;
+ *    qlen * max(0, max matrix entry) must be < 2^31 (SW_ERANGE otherwise).
+ *  - subject lengths >= 0 (a zero-length subject scores 0).
+ *  - top-k order: score descending, then global id ascending; slots past the
+ *    number of subjects are (id -1, score -1).
+ *
+ * Ownership / threading: all input pointers are borrowed for the duration of
+ * the call (sw_db_create copies and packs the database into device memory it
+ * owns).  Output buffers are caller-owned and left untouched on error.  One
+ * handle serialises its searches (internal mutex + stream ordering); distinct
+ * handles are independent.  All functions return SW_OK (0) or a negative
+ * status; sw_last_error() gives a thread-local message for the last failure.
+ */
+#ifndef SWSEARCH_H
+#define SWSEARCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SW_OK 0
+#define SW_EINVAL (-1)    /* invalid argument (message names the argument/position) */
+#define SW_ENOMEM (-2)    /* host or device allocation failed */
+#define SW_ECUDA (-3)     /* CUDA runtime error (message carries cudaGetErrorString) */
+#define SW_ERANGE (-4)    /* int32 score bound qlen * s_max < 2^31 violated */
+#define SW_EINTERNAL (-5) /* internal invariant violated */
+
+#define SW_NUM_CODES 24   /* real residue codes 0..23 */
+#define SW_DUMMY 24       /* internal padding code */
+#define SW_MATRIX_DIM 32
+
+typedef struct sw_db sw_db; /* opaque; owns its device memory */
+
+typedef struct sw_opts {
+  int32_t device;         /* CUDA device ordinal; -1 = the caller's current device */
+  int32_t first_stage;    /* lane width of the first pass: 8, 16 (default) or 32 */
+  int32_t long_threshold; /* subjects longer than this use the intra-task wavefront kernel;
+                             0 = library default, -1 = never (all inter-task) */
+  int32_t verbose;        /* 0 = silent */
+  int32_t reserved[4];    /* must be 0 */
+} sw_opts;
+
+typedef struct sw_stats {
+  int64_t cells;          /* qlen * sum of real subject lengths (GCUPS numerator) */
+  int64_t n_seqs;         /* subjects searched */
+  int64_t n_inter;        /* subjects aligned by the inter-task kernels */
+  int64_t n_intra;        /* subjects aligned by the intra-task kernel */
+  int64_t n_rerun16;      /* subjects re-aligned at int16 after an int8 first pass */
+  int64_t n_rerun32;      /* subjects re-aligned at int32 after saturating at int16 */
+  double seconds;         /* wall time of the search call */
+  double gcups;           /* cells / seconds / 1e9 */
+  float ms_profile, ms_inter, ms_rerun, ms_finalize; /* device times per stage (sw_search only) */
+  int32_t first_stage;    /* lane width actually used first */
+  int32_t reserved[7];
+} sw_stats;
+
+typedef struct sw_db_info {
+  int64_t n_seqs, n_residues;   /* real subjects / residues */
+  int64_t n_inter, n_intra;     /* split at long_threshold */
+  int64_t n_groups;             /* 64-subject interleaved groups of the inter-task layout */
+  int64_t packed_bytes;         /* device bytes of packed residues */
+  int64_t scratch_bytes;        /* device bytes of DP boundary scratch */
+  int64_t launches;             /* CUDA kernels launched by this handle so far */
+  int64_t n_searches;           /* searches enqueued so far */
+  int32_t max_len;              /* longest subject */
+  int32_t device;
+  int32_t long_threshold;
+  int32_t reserved[5];
+} sw_db_info;
+
+/* Fill *opts with defaults (device -1, first_stage 16, long_threshold 0). */
+void sw_opts_default(sw_opts* opts);
+
+/*
+ * Build a searchable database (the paper's offline index, and
+ * sequence profiles): stable sort by (length, input index),
+ * split at long_threshold, pack residues as 5-bit codes (6 per 32-bit word)
+ * interleaved over 64-subject groups, upload to the device.
+ *   residues   host, n_residues bytes, codes 0..23
+ *   offsets    host, n_seqs int64: subject i = residues[offsets[i] .. +lengths[i])
+ *   lengths    host, n_seqs int32 >= 0
+ *   global_ids host, n_seqs int64 in [0, 2^32-2], or NULL (= 0..n_seqs-1); used
+ *              only for top-k ids and the tie-break
+ *   opts       NULL = defaults
+ *   out        receives the handle (NULL on error)
+ */
+int sw_db_create(const uint8_t* residues, int64_t n_residues, const int64_t* offsets,
+                 const int32_t* lengths, int64_t n_seqs, const int64_t* global_ids,
+                 const sw_opts* opts, sw_db** out);
+
+/*
+ * Search one query against every subject; blocks until results are on the host.
+ *   query        host, qlen codes 0..23
+ *   matrix       host, 32*32 int8 (row = query residue)
+ *   k            >= 1
+ *   scores       host int32[n_seqs] in input order, or NULL
+ *   topk_ids     host int64[k] (global ids), or NULL
+ *   topk_scores  host int32[k], or NULL
+ *   stats        or NULL
+ */
+int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix,
+              int32_t alpha, int32_t beta, int32_t k, int32_t* scores, int64_t* topk_ids,
+              int32_t* topk_scores, sw_stats* stats);
+
+/*
+ * As sw_search, but enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ * stream) with DEVICE outputs and no host synchronisation.  query/matrix are
+ * host pointers, staged by the library.  d_scores int32[n_seqs] (input order),
+ * d_topk_ids int64[k], d_topk_scores int32[k]; any may be NULL.
+ */
+int sw_search_async(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix,
+                    int32_t alpha, int32_t beta, int32_t k, int32_t* d_scores,
+                    int64_t* d_topk_ids, int32_t* d_topk_scores, void* stream);
+
+/*
+ * Merge n_lists top-k lists (host; e.g. one per GPU after an all-gather) into
+ * the global top-k by (score desc, id asc).  Entries with id < 0 are ignored.
+ *   ids/scores   host, n_lists * k_in entries (list-major)
+ *   out_ids/out_scores  host, k_out entries; padded with (-1, -1)
+ */
+int sw_merge_topk(const int64_t* ids, const int32_t* scores, int32_t n_lists, int32_t k_in,
+                  int32_t k_out, int64_t* out_ids, int32_t* out_scores);
+
+int sw_db_get_info(const sw_db* db, sw_db_info* info);
+
+/*
+ * Device time (ms, CUDA events on the search's stream) of the four stages of
+ * the search enqueued `back` calls ago (1 = the latest; at most 64 back):
+ * ms[0] query profile, ms[1] first (int16x2 or int32) pass, ms[2] int32 rerun
+ * of saturated subjects, ms[3] scatter + top-k.  Waits for that search.
+ */
+int sw_db_stage_times(sw_db* db, int32_t back, float* ms);
+
+/* Release the handle and its device memory; NULL is a no-op. */
+void sw_db_destroy(sw_db* db);
+
+const char* sw_strerror(int status);
+const char* sw_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWSEARCH_H */

@@ -1,0 +1,218 @@
+"""paper_1404_4152_b200 — B200-native Smith-Waterman protein database search.
+
+Thin ctypes binding over the C ABI in include/swsearch.h (libswsearch.so,
+built in-tree for sm_100a).  Argument marshalling only: every step of the
+search runs in the library's CUDA kernels.  There is no CPU fallback: if the
+shared library is missing, importing this package raises.
+
+    db = Database(residues, offsets, lengths)            # sw_db_create
+    res = db.search(query, matrix, alpha=2, beta=12, k=10)   # sw_search
+    res.scores, res.topk_ids, res.topk_scores, res.stats
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libswsearch.so")
+
+SW_OK, SW_EINVAL, SW_ENOMEM, SW_ECUDA, SW_ERANGE, SW_EINTERNAL = 0, -1, -2, -3, -4, -5
+
+
+class SwError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class sw_opts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("first_stage", ctypes.c_int32),
+                ("long_threshold", ctypes.c_int32), ("verbose", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
+
+
+class sw_stats(ctypes.Structure):
+    _fields_ = [("cells", ctypes.c_int64), ("n_seqs", ctypes.c_int64), ("n_inter", ctypes.c_int64),
+                ("n_intra", ctypes.c_int64), ("n_rerun16", ctypes.c_int64), ("n_rerun32", ctypes.c_int64),
+                ("seconds", ctypes.c_double), ("gcups", ctypes.c_double),
+                ("ms_profile", ctypes.c_float), ("ms_inter", ctypes.c_float),
+                ("ms_rerun", ctypes.c_float), ("ms_finalize", ctypes.c_float),
+                ("first_stage", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+    def as_dict(self) -> dict:
+        return {f: (getattr(self, f) if f != "reserved" else None) for f, _ in self._fields_ if f != "reserved"}
+
+
+class sw_db_info(ctypes.Structure):
+    _fields_ = [("n_seqs", ctypes.c_int64), ("n_residues", ctypes.c_int64), ("n_inter", ctypes.c_int64),
+                ("n_intra", ctypes.c_int64), ("n_groups", ctypes.c_int64), ("packed_bytes", ctypes.c_int64),
+                ("scratch_bytes", ctypes.c_int64), ("launches", ctypes.c_int64), ("n_searches", ctypes.c_int64),
+                ("max_len", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("long_threshold", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+
+
+# Every symbol include/swsearch.h declares (tests check the .so exports all of them).
+EXPORTS = ("sw_opts_default", "sw_db_create", "sw_search", "sw_search_async", "sw_merge_topk",
+           "sw_db_get_info", "sw_db_stage_times", "sw_db_destroy", "sw_strerror", "sw_last_error")
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libswsearch.so; raises (no fallback) when it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.sw_opts_default.argtypes = [ctypes.POINTER(sw_opts)]
+        L.sw_opts_default.restype = None
+        L.sw_db_create.argtypes = [P, i64, P, P, i64, P, ctypes.POINTER(sw_opts), ctypes.POINTER(P)]
+        L.sw_db_create.restype = ctypes.c_int
+        L.sw_search.argtypes = [P, P, i32, P, i32, i32, i32, P, P, P, ctypes.POINTER(sw_stats)]
+        L.sw_search.restype = ctypes.c_int
+        L.sw_search_async.argtypes = [P, P, i32, P, i32, i32, i32, P, P, P, P]
+        L.sw_search_async.restype = ctypes.c_int
+        L.sw_merge_topk.argtypes = [P, P, i32, i32, i32, P, P]
+        L.sw_merge_topk.restype = ctypes.c_int
+        L.sw_db_get_info.argtypes = [P, ctypes.POINTER(sw_db_info)]
+        L.sw_db_get_info.restype = ctypes.c_int
+        L.sw_db_stage_times.argtypes = [P, i32, ctypes.POINTER(ctypes.c_float)]
+        L.sw_db_stage_times.restype = ctypes.c_int
+        L.sw_db_destroy.argtypes = [P]
+        L.sw_db_destroy.restype = None
+        L.sw_strerror.argtypes = [ctypes.c_int]
+        L.sw_strerror.restype = ctypes.c_char_p
+        L.sw_last_error.argtypes = []
+        L.sw_last_error.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != SW_OK:
+        L = lib()
+        raise SwError(rc, f"{L.sw_strerror(rc).decode()}: {L.sw_last_error().decode()}")
+
+
+def _ptr(a) -> int | None:
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+@dataclass
+class SearchResult:
+    scores: np.ndarray | None
+    topk_ids: np.ndarray
+    topk_scores: np.ndarray
+    stats: dict
+
+
+class Database:
+    """sw_db_create / sw_db_destroy.  Arrays are copied (and packed) by the library."""
+
+    def __init__(self, residues, offsets, lengths, global_ids=None, device: int = -1,
+                 first_stage: int = 16, long_threshold: int = 0):
+        L = lib()
+        res = np.ascontiguousarray(residues, dtype=np.uint8)
+        offs = np.ascontiguousarray(offsets, dtype=np.int64)
+        lens = np.ascontiguousarray(lengths, dtype=np.int32)
+        gids = None if global_ids is None else np.ascontiguousarray(global_ids, dtype=np.int64)
+        if offs.shape != lens.shape:
+            raise ValueError("offsets and lengths must have the same shape")
+        o = sw_opts()
+        L.sw_opts_default(ctypes.byref(o))
+        o.device, o.first_stage, o.long_threshold = device, first_stage, long_threshold
+        h = ctypes.c_void_p()
+        _check(L.sw_db_create(_ptr(res) if res.size else None, res.size, _ptr(offs) if offs.size else None,
+                              _ptr(lens) if lens.size else None, lens.size,
+                              None if gids is None else _ptr(gids), ctypes.byref(o), ctypes.byref(h)))
+        self._h = h
+        self.n_seqs = int(lens.size)
+
+    @classmethod
+    def from_synth(cls, db, **kw) -> "Database":
+        return cls(db.residues, db.offsets, db.lengths, **kw)
+
+    def info(self) -> dict:
+        i = sw_db_info()
+        _check(lib().sw_db_get_info(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in i._fields_ if f != "reserved"}
+
+    def stage_times(self, back: int = 1) -> list:
+        """[profile, first pass, rerun, ranking] device ms of the search `back` calls ago."""
+        ms = (ctypes.c_float * 4)()
+        _check(lib().sw_db_stage_times(self._h, back, ms))
+        return list(ms)
+
+    def search(self, query, matrix, alpha: int, beta: int, k: int = 10, scores: bool | np.ndarray = True,
+               topk_ids=None, topk_scores=None) -> SearchResult:
+        """Blocking search with host buffers (sw_search).  `scores` may be a
+        preallocated (e.g. pinned) int32 host array, True (allocate) or False."""
+        q = np.ascontiguousarray(query, dtype=np.uint8)
+        M = np.ascontiguousarray(matrix, dtype=np.int8)
+        if M.shape != (32, 32):
+            raise ValueError("matrix must be 32x32 int8 (see swdata.matrix32)")
+        if scores is True:
+            sc = np.empty(self.n_seqs, dtype=np.int32)
+        elif scores is False or scores is None:
+            sc = None
+        else:
+            sc = scores
+        ti = np.empty(k, dtype=np.int64) if topk_ids is None else topk_ids
+        ts = np.empty(k, dtype=np.int32) if topk_scores is None else topk_scores
+        st = sw_stats()
+        _check(lib().sw_search(self._h, _ptr(q), q.size, _ptr(M), alpha, beta, k, _ptr(sc), _ptr(ti),
+                               _ptr(ts), ctypes.byref(st)))
+        return SearchResult(sc, ti, ts, st.as_dict())
+
+    def search_async(self, query, matrix, alpha: int, beta: int, k: int, d_scores=None, d_topk_ids=None,
+                     d_topk_scores=None, stream=None):
+        """Enqueue on a CUDA stream (torch.cuda.Stream or raw handle) with device
+        outputs (torch tensors: int32[n], int64[k], int32[k]); no host sync."""
+        q = np.ascontiguousarray(query, dtype=np.uint8)
+        M = np.ascontiguousarray(matrix, dtype=np.int8)
+        if stream is None:
+            h = None
+        elif hasattr(stream, "cuda_stream"):
+            h = stream.cuda_stream
+        else:
+            h = int(stream)
+        _check(lib().sw_search_async(self._h, _ptr(q), q.size, _ptr(M), alpha, beta, k, _ptr(d_scores),
+                                     _ptr(d_topk_ids), _ptr(d_topk_scores), h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sw_db_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def merge_topk(ids: np.ndarray, scores: np.ndarray, k_out: int):
+    """sw_merge_topk over a (n_lists, k_in) stack of per-device top-k lists."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    scores = np.ascontiguousarray(scores, dtype=np.int32)
+    n_lists, k_in = ids.shape if ids.ndim == 2 else (1, ids.size)
+    oi = np.empty(k_out, dtype=np.int64)
+    os_ = np.empty(k_out, dtype=np.int32)
+    _check(lib().sw_merge_topk(_ptr(ids), _ptr(scores), n_lists, k_in, k_out, _ptr(oi), _ptr(os_)))
+    return oi, os_

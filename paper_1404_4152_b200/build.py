@@ -1,0 +1,45 @@
+"""Build the in-tree native libraries (sm_100a CUDA library + host helpers)."""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_1404_4152_b200")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread",
+           "-diag-suppress", "550"]
+SOURCES = [os.path.join(PKG, "csrc", "sw_api.cu")]
+DEPS = SOURCES + [os.path.join(PKG, "csrc", "sw_kernels.cuh"), os.path.join(ROOT, "include", "swsearch.h")]
+OUT = os.path.join(PKG, "libswsearch.so")
+
+
+def _stale(out, deps):
+    return not os.path.exists(out) or any(os.path.getmtime(d) > os.path.getmtime(out) for d in deps)
+
+
+def build_cuda(force=False, verbose=False):
+    if force or _stale(OUT, DEPS):
+        cmd = [NVCC, *ARCH, *NVFLAGS, "-shared", "-o", OUT, *SOURCES]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+    return OUT
+
+
+def build_swgen(force=False):
+    src = os.path.join(ROOT, "swdata", "swgen.c")
+    out = os.path.join(ROOT, "swdata", "_libswgen.so")
+    if force or _stale(out, [src]):
+        subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-pthread", "-o", out, src])
+    return out
+
+
+def build_all(force=False, verbose=False):
+    build_swgen(force)
+    return build_cuda(force, verbose)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, verbose="-v" in sys.argv)

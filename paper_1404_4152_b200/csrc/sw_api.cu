@@ -1,0 +1,697 @@
+// sw_api.cu — host side of the C ABI declared in include/swsearch.h.
+//
+// sw_db_create is the paper's offline indexing ("All subject
+// sequences are sorted in ascending order of sequence length") plus its
+// sequence-profile layout (consecutive sorted subjects
+// interleaved, padded with a dummy residue scoring 0).  sw_search runs the
+// four-stage workflow of PAPER.md:55 (Fig. 2) on one B200:
+//   (i) query profile -> (ii) inter-task alignment (int16x2 DPX, int32 rerun of
+//   flagged subjects) -> (iii) stream-ordered completion -> (iv) ranking
+//   (exact top-k by radix select).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../include/swsearch.h"
+#include "sw_kernels.cuh"
+
+using swk::GroupDesc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(_e == cudaErrorMemoryAllocation ? SW_ENOMEM : SW_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(_e), __FILE__, __LINE__);                     \
+  } while (0)
+
+constexpr int kTileRows = 64;        // query rows per register tile (int16x2 and int32 passes)
+constexpr int kMaxSmemProfile = 200 * 1024;
+
+int host_threads() {
+  unsigned n = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(n, 64u));
+}
+
+template <class F>
+void parallel_for(int64_t n, F f) {
+  int nt = host_threads();
+  if (n < 4096 || nt == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; t++) {
+    int64_t a = n * t / nt, b = n * (t + 1) / nt;
+    th.emplace_back([=] { f(a, b); });
+  }
+  for (auto& x : th) x.join();
+}
+
+}  // namespace
+
+struct sw_db {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  int first_stage = 16;
+  int long_threshold = -1;
+
+  int64_t n_seqs = 0, n_residues = 0, n_inter = 0, n_intra = 0, sum_len = 0;
+  int32_t max_len = 0, max_inter_len = 0;
+  int64_t n_groups = 0, n_words = 0;
+
+  uint2* d_words = nullptr;
+  GroupDesc* d_groups = nullptr;
+  int* d_perm = nullptr;          // sorted position -> input index
+  int* d_len_sorted = nullptr;    // sorted position -> length
+  long long* d_gid = nullptr;     // input index -> global id (nullptr: identity)
+
+  uint2* d_scratch = nullptr;     // DP boundary rows, one slab per resident warp
+  long long scratch_cols = 0;
+  int scratch_slots = 0;
+
+  // per-search buffers
+  uint8_t* d_query = nullptr;
+  int query_cap = 0;
+  int8_t* d_matrix = nullptr;
+  int8_t* d_prof = nullptr;
+  size_t prof_cap = 0;
+  int* d_score_sorted = nullptr;
+  int* d_scores = nullptr;        // input-order scores for the synchronous API
+  unsigned long long* d_keys = nullptr;
+  unsigned long long* d_cand = nullptr;
+  unsigned long long* d_cand2 = nullptr;
+  int cand_cap = 0;
+  int* d_flags = nullptr;         // flagged sorted positions
+  int* d_counters = nullptr;      // [0] inter work, [1] flag count, [2] rerun work, [3] cand count
+  unsigned* d_hist = nullptr;
+  swk::SelState* d_sel = nullptr;
+  long long* d_topk_ids = nullptr;
+  int* d_topk_scores = nullptr;
+  int topk_cap = 0;
+  void* d_cub = nullptr;
+  size_t cub_bytes = 0;
+
+  uint8_t* h_stage = nullptr;     // pinned staging for query + matrix
+  size_t stage_cap = 0;
+  cudaEvent_t ev_stage = nullptr, ev_done = nullptr;
+  // stage-boundary events of the last kRing searches (sync and async):
+  // [0] start, [1] profile done, [2] first pass done, [3] rerun done, [4] ranking done
+  static constexpr int kRing = 64;
+  cudaEvent_t ev_ring[kRing][5] = {};
+  int64_t n_searches = 0;
+  int64_t launches = 0;           // kernels launched by this handle (all searches)
+};
+
+extern "C" {
+
+void sw_opts_default(sw_opts* o) {
+  if (!o) return;
+  memset(o, 0, sizeof *o);
+  o->device = -1;
+  o->first_stage = 16;
+  o->long_threshold = 0;
+}
+
+const char* sw_strerror(int s) {
+  switch (s) {
+    case SW_OK: return "ok";
+    case SW_EINVAL: return "invalid argument";
+    case SW_ENOMEM: return "out of memory";
+    case SW_ECUDA: return "CUDA error";
+    case SW_ERANGE: return "score range exceeds int32 bound";
+    case SW_EINTERNAL: return "internal error";
+    default: return "unknown status";
+  }
+}
+
+const char* sw_last_error(void) { return g_last_error.c_str(); }
+
+static void free_db(sw_db* db) {
+  if (!db) return;
+  cudaSetDevice(db->device);
+  if (db->stream) cudaStreamSynchronize(db->stream);
+  void* ptrs[] = {db->d_words, db->d_groups, db->d_perm, db->d_len_sorted, db->d_gid, db->d_scratch,
+                  db->d_query, db->d_matrix, db->d_prof, db->d_score_sorted, db->d_scores, db->d_keys,
+                  db->d_cand, db->d_cand2, db->d_flags, db->d_counters, db->d_hist, db->d_sel,
+                  db->d_topk_ids, db->d_topk_scores, db->d_cub};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (db->h_stage) cudaFreeHost(db->h_stage);
+  if (db->ev_stage) cudaEventDestroy(db->ev_stage);
+  if (db->ev_done) cudaEventDestroy(db->ev_done);
+  for (auto& set : db->ev_ring)
+    for (auto& e : set)
+      if (e) cudaEventDestroy(e);
+  if (db->stream) cudaStreamDestroy(db->stream);
+  delete db;
+}
+
+void sw_db_destroy(sw_db* db) { free_db(db); }
+
+int sw_db_get_info(const sw_db* db, sw_db_info* info) {
+  if (!db || !info) return fail(SW_EINVAL, "sw_db_get_info: null argument");
+  memset(info, 0, sizeof *info);
+  info->n_seqs = db->n_seqs;
+  info->n_residues = db->sum_len;
+  info->n_inter = db->n_inter;
+  info->n_intra = db->n_intra;
+  info->n_groups = db->n_groups;
+  info->packed_bytes = db->n_words * (int64_t)sizeof(uint2);
+  info->scratch_bytes = (int64_t)db->scratch_slots * db->scratch_cols * 32 * (int64_t)sizeof(uint2);
+  info->max_len = db->max_len;
+  info->device = db->device;
+  info->long_threshold = db->long_threshold;
+  info->launches = db->launches;
+  info->n_searches = db->n_searches;
+  return SW_OK;
+}
+
+int sw_db_stage_times(sw_db* db, int32_t back, float* ms) {
+  if (!db || !ms) return fail(SW_EINVAL, "sw_db_stage_times: null argument");
+  if (back < 1 || back > sw_db::kRing || back > db->n_searches)
+    return fail(SW_EINVAL, "sw_db_stage_times: back must be in [1, min(%d, searches so far)]", sw_db::kRing);
+  cudaEvent_t* ev = db->ev_ring[(db->n_searches - back) % sw_db::kRing];
+  CK(cudaEventSynchronize(ev[4]));
+  for (int t = 0; t < 4; t++) CK(cudaEventElapsedTime(&ms[t], ev[t], ev[t + 1]));
+  return SW_OK;
+}
+
+static int validate_db(const uint8_t* residues, int64_t n_residues, const int64_t* offsets,
+                       const int32_t* lengths, int64_t n_seqs, const int64_t* gids) {
+  // ---- validation (host) ----
+  if (n_seqs < 0 || n_seqs > 0x7fffffffLL - 64) return fail(SW_EINVAL, "n_seqs out of range: %lld", (long long)n_seqs);
+  if (n_residues < 0) return fail(SW_EINVAL, "n_residues < 0");
+  if (n_seqs > 0 && (!offsets || !lengths)) return fail(SW_EINVAL, "offsets/lengths must be non-NULL");
+  if (n_residues > 0 && !residues) return fail(SW_EINVAL, "residues must be non-NULL");
+  std::atomic<int64_t> bad{-1};
+  std::atomic<int> bad_kind{0};
+  parallel_for(n_seqs, [&](int64_t a, int64_t b) {
+    for (int64_t i = a; i < b && bad.load(std::memory_order_relaxed) < 0; i++) {
+      const int64_t off = offsets[i];
+      const int32_t len = lengths[i];
+      if (len < 0 || off < 0 || off > n_residues || (int64_t)len > n_residues - off) {
+        bad = i; bad_kind = 1; return;
+      }
+      const uint8_t* s = residues + off;
+      for (int32_t p = 0; p < len; p++)
+        if (s[p] >= SW_NUM_CODES) { bad = i; bad_kind = 2; return; }
+      if (gids && (gids[i] < 0 || gids[i] > 0xfffffffeLL)) { bad = i; bad_kind = 3; return; }
+    }
+  });
+  if (bad >= 0) {
+    const int64_t i = bad;
+    if (bad_kind == 1) return fail(SW_EINVAL, "subject %lld: offset %lld / length %d outside residues[0,%lld)", (long long)i, (long long)offsets[i], lengths[i], (long long)n_residues);
+    if (bad_kind == 2) return fail(SW_EINVAL, "subject %lld: residue code >= 24", (long long)i);
+    return fail(SW_EINVAL, "subject %lld: global id %lld outside [0, 2^32-2]", (long long)i, (long long)gids[i]);
+  }
+  return SW_OK;
+}
+
+static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_t* offsets,
+                       const int32_t* lengths, int64_t n_seqs, const int64_t* gids, const sw_opts* o,
+                       sw_db* db) {
+  db->n_seqs = n_seqs;
+  db->n_residues = n_residues;
+
+  // ---- stable sort by (length, input index): counting sort ----
+  int32_t max_len = 0;
+  int64_t sum_len = 0;
+  for (int64_t i = 0; i < n_seqs; i++) {
+    max_len = std::max(max_len, lengths[i]);
+    sum_len += lengths[i];
+  }
+  db->max_len = max_len;
+  db->sum_len = sum_len;
+  std::vector<int> perm(n_seqs);
+  {
+    std::vector<int64_t> cnt((size_t)max_len + 2, 0);
+    for (int64_t i = 0; i < n_seqs; i++) cnt[(size_t)lengths[i] + 1]++;
+    for (size_t l = 1; l < cnt.size(); l++) cnt[l] += cnt[l - 1];
+    for (int64_t i = 0; i < n_seqs; i++) perm[cnt[(size_t)lengths[i]]++] = (int)i;
+  }
+  std::vector<int> len_sorted(n_seqs);
+  for (int64_t p = 0; p < n_seqs; p++) len_sorted[p] = lengths[perm[p]];
+
+  // ---- inter/intra split (the intra-task kernel takes subjects > threshold) ----
+  db->long_threshold = o->long_threshold;
+  int64_t n_inter = n_seqs;
+  if (db->long_threshold > 0)
+    n_inter = std::upper_bound(len_sorted.begin(), len_sorted.end(), db->long_threshold) - len_sorted.begin();
+  db->n_inter = n_inter;
+  db->n_intra = n_seqs - n_inter;
+  if (db->n_intra > 0) return fail(SW_EINVAL, "long_threshold: intra-task kernel not available in this build");
+  db->max_inter_len = n_inter ? len_sorted[n_inter - 1] : 0;
+
+  // ---- groups of 64 consecutive sorted subjects, 5-bit codes, 6 per word ----
+  const int64_t n_groups = (n_inter + swk::kGroup - 1) / swk::kGroup;
+  std::vector<GroupDesc> groups(n_groups);
+  int64_t base = 0;
+  for (int64_t g = 0; g < n_groups; g++) {
+    const int64_t first = g * swk::kGroup, last = std::min(first + swk::kGroup, n_inter) - 1;
+    groups[g].base = base;
+    groups[g].ncols = len_sorted[last];
+    groups[g].count = (int)(last - first + 1);
+    const int64_t nw = (groups[g].ncols + swk::kResPerWord - 1) / swk::kResPerWord;
+    base += nw * 32;
+  }
+  db->n_groups = n_groups;
+  db->n_words = base;
+
+  CK(cudaMalloc(&db->d_words, std::max<int64_t>(base, 1) * sizeof(uint2)));
+  {
+    // pack group ranges into two pinned staging buffers, upload overlapped
+    const int64_t kChunkWords = 1 << 24;   // 128 MB of uint2
+    uint2* stage[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2];
+    CK(cudaHostAlloc(&stage[0], kChunkWords * sizeof(uint2), cudaHostAllocDefault));
+    CK(cudaHostAlloc(&stage[1], kChunkWords * sizeof(uint2), cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    int64_t g0 = 0;
+    int buf = 0;
+    bool used[2] = {false, false};
+    int rc = SW_OK;
+    while (g0 < n_groups && rc == SW_OK) {
+      int64_t g1 = g0;
+      while (g1 < n_groups) {
+        const int64_t end = (g1 + 1 < n_groups ? groups[g1 + 1].base : base);
+        if (end - groups[g0].base > kChunkWords && g1 > g0) break;
+        if (end - groups[g0].base > kChunkWords) { rc = fail(SW_EINTERNAL, "group larger than staging"); break; }
+        g1++;
+      }
+      if (rc != SW_OK) break;
+      if (used[buf]) cudaEventSynchronize(ev[buf]);
+      uint2* st = stage[buf];
+      const int64_t wbase = groups[g0].base;
+      const int64_t wend = (g1 < n_groups ? groups[g1].base : base);
+      parallel_for(g1 - g0, [&](int64_t a, int64_t b) {
+        for (int64_t gg = g0 + a; gg < g0 + b; gg++) {
+          const GroupDesc& G = groups[gg];
+          const int nw = (G.ncols + swk::kResPerWord - 1) / swk::kResPerWord;
+          uint2* out = st + (G.base - wbase);
+          for (int l = 0; l < swk::kGroup; l++) {
+            const int64_t p = gg * swk::kGroup + l;
+            const uint8_t* s = nullptr;
+            int len = 0;
+            if (l < G.count) {
+              s = residues + offsets[perm[p]];
+              len = len_sorted[p];
+            }
+            for (int w = 0; w < nw; w++) {
+              uint32_t word = 0;
+              for (int c = 0; c < swk::kResPerWord; c++) {
+                const int j = w * swk::kResPerWord + c;
+                const uint32_t code = j < len ? s[j] : (uint32_t)swk::kDummy;
+                word |= code << (5 * c);
+              }
+              uint2& dst = out[(int64_t)w * 32 + (l >> 1)];
+              if (l & 1) dst.y = word; else dst.x = word;
+            }
+          }
+        }
+      });
+      cudaError_t e = cudaMemcpyAsync(db->d_words + wbase, st, (wend - wbase) * sizeof(uint2),
+                                      cudaMemcpyHostToDevice, db->stream);
+      if (e != cudaSuccess) { rc = fail(SW_ECUDA, "upload: %s", cudaGetErrorString(e)); break; }
+      cudaEventRecord(ev[buf], db->stream);
+      used[buf] = true;
+      buf ^= 1;
+      g0 = g1;
+    }
+    cudaStreamSynchronize(db->stream);
+    cudaFreeHost(stage[0]);
+    cudaFreeHost(stage[1]);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    if (rc != SW_OK) return rc;
+  }
+  CK(cudaMalloc(&db->d_groups, std::max<int64_t>(n_groups, 1) * sizeof(GroupDesc)));
+  if (n_groups) CK(cudaMemcpy(db->d_groups, groups.data(), n_groups * sizeof(GroupDesc), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&db->d_perm, std::max<int64_t>(n_seqs, 1) * sizeof(int)));
+  CK(cudaMalloc(&db->d_len_sorted, std::max<int64_t>(n_seqs, 1) * sizeof(int)));
+  if (n_seqs) {
+    CK(cudaMemcpy(db->d_perm, perm.data(), n_seqs * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(db->d_len_sorted, len_sorted.data(), n_seqs * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  if (gids && n_seqs) {
+    CK(cudaMalloc(&db->d_gid, n_seqs * sizeof(long long)));
+    CK(cudaMemcpy(db->d_gid, gids, n_seqs * sizeof(long long), cudaMemcpyHostToDevice));
+  }
+
+  // ---- DP boundary scratch: one slab per resident warp of the persistent kernels ----
+  db->scratch_slots = db->num_sms * (swk::kInterThreads / 32);
+  db->scratch_cols = ((int64_t)db->max_inter_len + swk::kResPerWord) / swk::kResPerWord * swk::kResPerWord + swk::kResPerWord;
+  CK(cudaMalloc(&db->d_scratch, (size_t)db->scratch_slots * db->scratch_cols * 32 * sizeof(uint2)));
+
+  // ---- per-search buffers sized by n ----
+  const int64_t n1 = std::max<int64_t>(n_seqs, 1);
+  CK(cudaMalloc(&db->d_score_sorted, n1 * sizeof(int)));
+  CK(cudaMalloc(&db->d_scores, n1 * sizeof(int)));
+  CK(cudaMalloc(&db->d_keys, n1 * sizeof(unsigned long long)));
+  CK(cudaMalloc(&db->d_flags, n1 * sizeof(int)));
+  CK(cudaMalloc(&db->d_counters, 8 * sizeof(int)));
+  CK(cudaMalloc(&db->d_hist, 256 * sizeof(unsigned)));
+  CK(cudaMemset(db->d_hist, 0, 256 * sizeof(unsigned)));
+  CK(cudaMalloc(&db->d_sel, sizeof(swk::SelState)));
+  CK(cudaMalloc(&db->d_matrix, 32 * 32));
+  CK(cudaEventCreateWithFlags(&db->ev_stage, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&db->ev_done, cudaEventDisableTiming));
+  for (auto& set : db->ev_ring)
+    for (auto& e : set) CK(cudaEventCreate(&e));
+  return SW_OK;
+}
+
+int sw_db_create(const uint8_t* residues, int64_t n_residues, const int64_t* offsets,
+                 const int32_t* lengths, int64_t n_seqs, const int64_t* global_ids,
+                 const sw_opts* opts, sw_db** out) {
+  if (!out) return fail(SW_EINVAL, "out must be non-NULL");
+  *out = nullptr;
+  sw_opts o;
+  sw_opts_default(&o);
+  if (opts) o = *opts;
+  if (o.first_stage != 8 && o.first_stage != 16 && o.first_stage != 32)
+    return fail(SW_EINVAL, "first_stage must be 8, 16 or 32 (got %d)", o.first_stage);
+  if (o.first_stage == 8) return fail(SW_EINVAL, "first_stage 8: int8 stage not available in this build");
+  if (o.long_threshold == 0) o.long_threshold = -1;   // default: all subjects inter-task (this build)
+  {
+    int rc = validate_db(residues, n_residues, offsets, lengths, n_seqs, global_ids);
+    if (rc != SW_OK) return rc;
+  }
+  sw_db* db = new (std::nothrow) sw_db;
+  if (!db) return fail(SW_ENOMEM, "host allocation");
+  if (o.device < 0) {
+    if (cudaGetDevice(&db->device) != cudaSuccess) { delete db; return fail(SW_ECUDA, "cudaGetDevice failed"); }
+  } else {
+    db->device = o.device;
+  }
+  db->first_stage = o.first_stage;
+  cudaError_t e = cudaSetDevice(db->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&db->num_sms, cudaDevAttrMultiProcessorCount, db->device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&db->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    int rc = fail(SW_ECUDA, "device %d: %s", db->device, cudaGetErrorString(e));
+    free_db(db);
+    return rc;
+  }
+  int rc = create_impl(residues, n_residues, offsets, lengths, n_seqs, global_ids, &o, db);
+  if (rc != SW_OK) {
+    std::string msg = g_last_error;
+    free_db(db);
+    g_last_error = msg;
+    return rc;
+  }
+  *out = db;
+  return SW_OK;
+}
+
+static int validate_search(const sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix,
+                           int32_t alpha, int32_t beta, int32_t k, int* smax_out) {
+  if (!db) return fail(SW_EINVAL, "db is NULL");
+  if (!query || !matrix) return fail(SW_EINVAL, "query/matrix must be non-NULL");
+  if (qlen < 1) return fail(SW_EINVAL, "qlen must be >= 1 (got %d)", qlen);
+  if (k < 1) return fail(SW_EINVAL, "k must be >= 1 (got %d)", k);
+  if (alpha < 0 || beta < alpha || beta > 32767)
+    return fail(SW_EINVAL, "need 0 <= alpha <= beta <= 32767 (alpha=%d, beta=%d)", alpha, beta);
+  for (int i = 0; i < qlen; i++)
+    if (query[i] >= SW_NUM_CODES) return fail(SW_EINVAL, "query position %d: residue code %d >= 24", i, query[i]);
+  int smax = 0;
+  for (int r = 0; r < 32; r++)
+    for (int c = 0; c < 32; c++) {
+      const int v = matrix[r * 32 + c];
+      if ((r >= SW_NUM_CODES || c >= SW_NUM_CODES) && v != 0)
+        return fail(SW_EINVAL, "matrix[%d][%d] = %d: rows/columns 24..31 must be 0", r, c, v);
+      smax = std::max(smax, v);
+    }
+  if ((int64_t)qlen * smax >= (1LL << 31)) return fail(SW_ERANGE, "qlen * s_max = %lld >= 2^31", (long long)qlen * smax);
+  *smax_out = smax;
+  return SW_OK;
+}
+
+static int ensure(void** p, size_t* cap, size_t need) {
+  if (*cap >= need && *p) return SW_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  CK(cudaMalloc(p, need));
+  *cap = need;
+  return SW_OK;
+}
+
+// Enqueue the whole search on `st`.  Outputs: d_scores (input order) may be
+// nullptr; top-k always goes to d_tk_ids/d_tk_scores when non-null.
+static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix,
+                          int32_t alpha, int32_t beta, int32_t k, int smax, int* d_scores,
+                          long long* d_tk_ids, int* d_tk_scores, cudaStream_t st) {
+  cudaEvent_t* ev = db->ev_ring[db->n_searches % sw_db::kRing];
+  int64_t nl = 0;   // kernel launches of this search
+  // ---- stage (i): query + matrix H2D and profile ----
+  const int m_pad = (qlen + 7) / 8 * 8;
+  const int stride = (m_pad + 31) / 32 * 32 + 8;   // 8-byte skew per residue row (bank spread)
+  const size_t prof_bytes = ((size_t)swk::kProfRows * stride + 15) / 16 * 16;
+  {
+    const size_t need = (size_t)qlen + 1024;
+    if (db->stage_cap < need) {
+      if (db->h_stage) { cudaEventSynchronize(db->ev_stage); cudaFreeHost(db->h_stage); db->h_stage = nullptr; }
+      CK(cudaHostAlloc(&db->h_stage, need, cudaHostAllocDefault));
+      db->stage_cap = need;
+    } else {
+      CK(cudaEventSynchronize(db->ev_stage));   // previous staged copy has drained
+    }
+    memcpy(db->h_stage, matrix, 1024);
+    memcpy(db->h_stage + 1024, query, qlen);
+    size_t qcap = (size_t)db->query_cap;
+    void* dq = db->d_query;
+    int rc = ensure(&dq, &qcap, (size_t)qlen);
+    db->d_query = (uint8_t*)dq;
+    db->query_cap = (int)qcap;
+    if (rc) return rc;
+    void* dp = db->d_prof;
+    rc = ensure(&dp, &db->prof_cap, prof_bytes);
+    db->d_prof = (int8_t*)dp;
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(db->d_matrix, db->h_stage, 1024, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(db->d_query, db->h_stage + 1024, qlen, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(db->ev_stage, st));
+  }
+  CK(cudaEventRecord(ev[0], st));
+  nl++;
+  swk::k_profile<<<64, 256, 0, st>>>(db->d_query, qlen, db->d_matrix, db->d_prof, stride);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(db->d_counters, 0, 8 * sizeof(int), st));
+  CK(cudaEventRecord(ev[1], st));
+
+  // ---- stage (ii): alignment ----
+  const int n = (int)db->n_seqs;
+  const bool smem = prof_bytes <= (size_t)kMaxSmemProfile;
+  const size_t smem_bytes = smem ? prof_bytes : 0;
+  const int grid = db->num_sms;   // one persistent 384-thread CTA per SM
+  const int limit16 = 32767 - smax;
+  if (db->n_inter > 0) {
+    if (db->first_stage == 16) {
+      auto kern = smem ? swk::k_inter16<kTileRows, true> : swk::k_inter16<kTileRows, false>;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
+      kern<<<grid, swk::kInterThreads, smem_bytes, st>>>(
+          db->d_words, db->d_groups, (int)db->n_groups, db->d_prof, m_pad, stride, alpha, beta, limit16,
+          db->d_scratch, db->scratch_cols, db->d_counters + 0, db->d_score_sorted, db->d_counters + 1,
+          db->d_flags);
+      CK(cudaGetLastError());
+      nl++;
+    }
+    CK(cudaEventRecord(ev[2], st));
+    auto k32 = smem ? swk::k_list32<kTileRows, true> : swk::k_list32<kTileRows, false>;
+    CK(cudaFuncSetAttribute(k32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
+    if (db->first_stage == 16) {
+      // rerun only the subjects flagged by the int16 pass (count read on device)
+      k32<<<grid, swk::kInterThreads, smem_bytes, st>>>(
+          db->d_words, db->d_groups, db->d_flags, db->d_counters + 1, 0, db->d_len_sorted, db->d_prof,
+          m_pad, stride, alpha, beta, db->d_scratch, db->scratch_cols, db->d_counters + 2,
+          db->d_score_sorted);
+    } else {
+      k32<<<grid, swk::kInterThreads, smem_bytes, st>>>(
+          db->d_words, db->d_groups, nullptr, nullptr, (int)db->n_inter, db->d_len_sorted, db->d_prof,
+          m_pad, stride, alpha, beta, db->d_scratch, db->scratch_cols, db->d_counters + 2,
+          db->d_score_sorted);
+    }
+    CK(cudaGetLastError());
+    nl++;
+  } else {
+    CK(cudaEventRecord(ev[2], st));
+  }
+  CK(cudaEventRecord(ev[3], st));
+
+  // ---- stage (iv): scatter + exact top-k ----
+  if (n > 0) {
+    const int fb = std::min((n + 255) / 256, db->num_sms * 8);
+    swk::k_finalize<<<fb, 256, 0, st>>>(db->d_score_sorted, db->d_perm, n, db->d_gid, d_scores, db->d_keys);
+    CK(cudaGetLastError());
+    nl++;
+  }
+  if (d_tk_ids || d_tk_scores) {
+    const int cnt = std::min<int64_t>(k, n);
+    if (cnt > 0) {
+      const bool take_all = k >= n;
+      if (!take_all) {
+        swk::SelState s0{0ull, 0ull, (long long)k};
+        CK(cudaMemcpyAsync(db->d_sel, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+        const int hb = std::min((n + 1023) / 1024, db->num_sms * 4);
+        for (int shift = 56; shift >= 0; shift -= 8) {
+          swk::k_sel_hist<<<hb, 256, 0, st>>>(db->d_keys, n, db->d_sel, shift, db->d_hist);
+          swk::k_sel_pick<<<1, 256, 0, st>>>(db->d_sel, shift, db->d_hist);
+          nl += 2;
+        }
+        CK(cudaGetLastError());
+      }
+      if (db->cand_cap < cnt) {
+        if (db->d_cand) cudaFree(db->d_cand);
+        if (db->d_cand2) cudaFree(db->d_cand2);
+        db->d_cand = db->d_cand2 = nullptr;
+        CK(cudaMalloc(&db->d_cand, (size_t)cnt * sizeof(unsigned long long)));
+        CK(cudaMalloc(&db->d_cand2, (size_t)cnt * sizeof(unsigned long long)));
+        db->cand_cap = cnt;
+      }
+      const int cb = std::min((n + 1023) / 1024, db->num_sms * 4);
+      swk::k_sel_compact<<<cb, 256, 0, st>>>(db->d_keys, n, db->d_sel, take_all ? 1 : 0, db->d_cand,
+                                            db->d_counters + 3);
+      CK(cudaGetLastError());
+      nl += 2;   // compaction + final sort/decode
+      if (cnt <= 4096) {
+        swk::k_topk_small<<<1, 1024, 0, st>>>(db->d_cand, cnt, k, d_tk_ids, d_tk_scores);
+      } else {
+        size_t need = 0;
+        cub::DeviceRadixSort::SortKeysDescending(nullptr, need, db->d_cand, db->d_cand2, cnt, 0, 64, st);
+        int rc = ensure(&db->d_cub, &db->cub_bytes, need);
+        if (rc) return rc;
+        CK(cub::DeviceRadixSort::SortKeysDescending(db->d_cub, need, db->d_cand, db->d_cand2, cnt, 0, 64, st));
+        swk::k_topk_decode<<<(k + 255) / 256, 256, 0, st>>>(db->d_cand2, cnt, k, d_tk_ids, d_tk_scores);
+      }
+      CK(cudaGetLastError());
+    } else {
+      swk::k_topk_decode<<<(k + 255) / 256, 256, 0, st>>>(db->d_cand, 0, k, d_tk_ids, d_tk_scores);
+      CK(cudaGetLastError());
+      nl++;
+    }
+  }
+  CK(cudaEventRecord(ev[4], st));
+  CK(cudaEventRecord(db->ev_done, st));
+  db->n_searches++;
+  db->launches += nl;
+  return SW_OK;
+}
+
+int sw_search_async(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix, int32_t alpha,
+                    int32_t beta, int32_t k, int32_t* d_scores, int64_t* d_topk_ids,
+                    int32_t* d_topk_scores, void* stream) {
+  int smax = 0;
+  int rc = validate_search(db, query, qlen, matrix, alpha, beta, k, &smax);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(db->mu);
+  CK(cudaSetDevice(db->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaStreamWaitEvent(st, db->ev_done, 0));   // serialise with the previous search on this handle
+  return search_enqueue(db, query, qlen, matrix, alpha, beta, k, smax, d_scores, (long long*)d_topk_ids,
+                        d_topk_scores, st);
+}
+
+int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix, int32_t alpha,
+              int32_t beta, int32_t k, int32_t* scores, int64_t* topk_ids, int32_t* topk_scores,
+              sw_stats* stats) {
+  const auto t0 = std::chrono::steady_clock::now();
+  int smax = 0;
+  int rc = validate_search(db, query, qlen, matrix, alpha, beta, k, &smax);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(db->mu);
+  CK(cudaSetDevice(db->device));
+  {
+    if (db->topk_cap < k) {
+      if (db->d_topk_ids) cudaFree(db->d_topk_ids);
+      if (db->d_topk_scores) cudaFree(db->d_topk_scores);
+      db->d_topk_ids = nullptr;
+      db->d_topk_scores = nullptr;
+      CK(cudaMalloc(&db->d_topk_ids, (size_t)k * sizeof(long long)));
+      CK(cudaMalloc(&db->d_topk_scores, (size_t)k * sizeof(int)));
+      db->topk_cap = k;
+    }
+  }
+  cudaStream_t st = db->stream;
+  rc = search_enqueue(db, query, qlen, matrix, alpha, beta, k, smax, db->d_scores, db->d_topk_ids,
+                      db->d_topk_scores, st);
+  if (rc) return rc;
+  if (scores && db->n_seqs)
+    CK(cudaMemcpyAsync(scores, db->d_scores, db->n_seqs * sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (topk_ids) CK(cudaMemcpyAsync(topk_ids, db->d_topk_ids, (size_t)k * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  if (topk_scores) CK(cudaMemcpyAsync(topk_scores, db->d_topk_scores, (size_t)k * sizeof(int), cudaMemcpyDeviceToHost, st));
+  int counters[8] = {0};
+  CK(cudaMemcpyAsync(counters, db->d_counters, sizeof counters, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const auto t1 = std::chrono::steady_clock::now();
+  if (stats) {
+    memset(stats, 0, sizeof *stats);
+    stats->cells = (int64_t)qlen * db->sum_len;
+    stats->n_seqs = db->n_seqs;
+    stats->n_inter = db->n_inter;
+    stats->n_intra = db->n_intra;
+    stats->n_rerun32 = db->first_stage == 16 ? counters[1] : 0;
+    stats->seconds = std::chrono::duration<double>(t1 - t0).count();
+    stats->gcups = stats->seconds > 0 ? (double)stats->cells / stats->seconds / 1e9 : 0.0;
+    cudaEvent_t* ev = db->ev_ring[(db->n_searches - 1) % sw_db::kRing];
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[0], ev[1]); stats->ms_profile = ms;
+    cudaEventElapsedTime(&ms, ev[1], ev[2]); stats->ms_inter = ms;
+    cudaEventElapsedTime(&ms, ev[2], ev[3]); stats->ms_rerun = ms;
+    cudaEventElapsedTime(&ms, ev[3], ev[4]); stats->ms_finalize = ms;
+    stats->first_stage = db->first_stage;
+  }
+  return SW_OK;
+}
+
+// Host merge of per-device top-k lists (the multi-GPU exchange step, DESIGN.md §"Multi-GPU").
+int sw_merge_topk(const int64_t* ids, const int32_t* scores, int32_t n_lists, int32_t k_in, int32_t k_out,
+                  int64_t* out_ids, int32_t* out_scores) {
+  if (n_lists < 0 || k_in < 0 || k_out < 1) return fail(SW_EINVAL, "sw_merge_topk: bad sizes");
+  if ((n_lists * (int64_t)k_in > 0 && (!ids || !scores)) || !out_ids || !out_scores)
+    return fail(SW_EINVAL, "sw_merge_topk: null pointer");
+  std::vector<std::pair<int32_t, int64_t>> all;
+  all.reserve((size_t)n_lists * k_in);
+  for (int64_t t = 0; t < (int64_t)n_lists * k_in; t++)
+    if (ids[t] >= 0) all.emplace_back(scores[t], ids[t]);
+  const size_t take = std::min<size_t>(all.size(), (size_t)k_out);
+  std::partial_sort(all.begin(), all.begin() + take, all.end(), [](const auto& a, const auto& b) {
+    return a.first != b.first ? a.first > b.first : a.second < b.second;
+  });
+  for (int32_t t = 0; t < k_out; t++) {
+    out_ids[t] = (size_t)t < take ? all[t].second : -1;
+    out_scores[t] = (size_t)t < take ? all[t].first : -1;
+  }
+  return SW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/swsearch.h declares, rejects invalid inputs before touching
+the device, and merges top-k lists (host function) as the oracle ranks."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1404_4152_b200 as sw
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    txt = open(os.path.join(ROOT, "include", "swsearch.h")).read()
+    return set(re.findall(r"^\S[^\n(]*?\b(sw_\w+)\s*\(", txt, flags=re.M))
+
+
+def test_header_and_binding_agree():
+    assert _declared() == set(sw.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = sw.lib()
+    for name in _declared():
+        assert hasattr(L, name), name
+    out = os.popen(f"nm -D --defined-only {sw.LIB_PATH}").read()
+    for name in _declared():
+        assert re.search(rf"\bT {name}\b", out), f"{name} not exported"
+
+
+def test_strerror():
+    L = sw.lib()
+    assert L.sw_strerror(0) == b"ok"
+    assert L.sw_strerror(-1) == b"invalid argument"
+    assert L.sw_strerror(-4).startswith(b"score range")
+
+
+def _create(res, offs, lens, gids=None, **kw):
+    return sw.Database(res, offs, lens, global_ids=gids, **kw)
+
+
+@pytest.mark.parametrize("case", ["bad_code", "overrun", "neg_len", "bad_gid", "bad_stage"])
+def test_db_create_validation(case):
+    res = np.array([0, 1, 2, 3, 4, 5], dtype=np.uint8)
+    offs = np.array([0, 3], dtype=np.int64)
+    lens = np.array([3, 3], dtype=np.int32)
+    gids = None
+    kw = {}
+    if case == "bad_code":
+        res[4] = 24
+    elif case == "overrun":
+        lens[1] = 4
+    elif case == "neg_len":
+        lens[0] = -1
+    elif case == "bad_gid":
+        gids = np.array([0, 1 << 33], dtype=np.int64)
+    elif case == "bad_stage":
+        kw["first_stage"] = 12
+    with pytest.raises(sw.SwError) as ei:
+        _create(res, offs, lens, gids, **kw)
+    assert ei.value.code == sw.SW_EINVAL
+
+
+def test_merge_topk_matches_oracle_ranking():
+    rng = np.random.default_rng(0)
+    lists_ids, lists_sc = [], []
+    all_ids, all_sc = [], []
+    for r in range(4):
+        ids = np.arange(r, 400, 4)
+        sc = rng.integers(0, 30, size=ids.size).astype(np.int32)
+        all_ids.append(ids)
+        all_sc.append(sc)
+        ti, ts = oracle.topk(sc, 12, ids)
+        lists_ids.append(ti)
+        lists_sc.append(ts)
+    mi, ms = sw.merge_topk(np.stack(lists_ids), np.stack(lists_sc), 12)
+    ri, rs = oracle.topk(np.concatenate(all_sc), 12, np.concatenate(all_ids))
+    assert np.array_equal(mi, ri) and np.array_equal(ms, rs)
+    mi, ms = sw.merge_topk(np.array([[3, -1]]), np.array([[7, -1]]), 3)
+    assert mi.tolist() == [3, -1, -1] and ms.tolist() == [7, -1, -1]

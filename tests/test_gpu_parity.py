@@ -1,0 +1,195 @@
+"""GPU parity: every score from the CUDA path (through the C ABI) equals the
+oracle bit-exactly; the top-k equals the oracle's full-sort ranking.
+
+Small cases cover every subject exhaustively (several query tiles, ragged
+tails, word/tile boundaries, degenerate parameters, saturation limits).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1404_4152_b200 as sw
+from swdata import blosum50, blosum62, matrix32, random_db, stream_key
+from swdata.synth import gen_residues
+
+pytestmark = pytest.mark.gpu
+
+B62 = matrix32(blosum62())
+B50 = matrix32(blosum50())
+
+
+def _query(m, seed=0):
+    return gen_residues(stream_key(seed, "test-query", m), 0, m)
+
+
+def _check(db, q, M, alpha, beta, k=10, first_stage=16, gids=None, **kw):
+    with sw.Database(db.residues, db.offsets, db.lengths, global_ids=gids, device=0,
+                     first_stage=first_stage, **kw) as g:
+        res = g.search(q, M, alpha, beta, k=k)
+    ref = oracle.db_scores(q, db, M, alpha, beta)
+    bad = np.nonzero(res.scores != ref)[0]
+    assert bad.size == 0, (f"{bad.size}/{ref.size} differ; first id {bad[0]} len {db.lengths[bad[0]]}: "
+                           f"gpu {res.scores[bad[0]]} oracle {ref[bad[0]]}")
+    ti, ts = oracle.topk(ref, k, gids)
+    assert np.array_equal(res.topk_scores, ts)
+    assert np.array_equal(res.topk_ids, ti)
+    return res
+
+
+def test_lengths_0_to_300_exhaustive():
+    db = random_db(1, np.arange(0, 301))
+    for m in (1, 7, 8, 9, 63, 64, 65, 144):
+        _check(db, _query(m), B62, 2, 12)
+
+
+@pytest.mark.parametrize("m", [127, 128, 129, 191, 200, 464, 1000])
+def test_query_tiles_and_ragged_tail(m):
+    rng = np.random.default_rng(m)
+    lens = np.concatenate([rng.integers(0, 700, size=900), [5, 6, 7, 11, 12, 13, 1, 0]])
+    _check(random_db(m, lens), _query(m, 1), B62, 2, 12)
+
+
+@pytest.mark.parametrize("alpha,beta", [(0, 0), (1, 1), (2, 12), (1, 12), (5, 40), (0, 30), (3, 32767)])
+def test_gap_parameters(alpha, beta):
+    rng = np.random.default_rng(alpha * 100 + beta)
+    db = random_db(7, rng.integers(1, 400, size=700))
+    _check(db, _query(300, 2), B62, alpha, beta)
+
+
+def test_blosum50_and_random_asymmetric_matrices():
+    rng = np.random.default_rng(3)
+    db = random_db(8, rng.integers(1, 500, size=600))
+    _check(db, _query(250, 3), B50, 2, 12)
+    for t in range(3):
+        M = np.zeros((32, 32), dtype=np.int8)
+        M[:24, :24] = rng.integers(-128 if t == 0 else -10, 128 if t == 0 else 12, size=(24, 24))
+        _check(db, _query(180, 4 + t), M, 1 + t, 10 + 3 * t)
+
+
+def test_first_stage_32_equals_oracle():
+    rng = np.random.default_rng(4)
+    db = random_db(9, rng.integers(0, 600, size=800))
+    _check(db, _query(333, 5), B62, 2, 12, first_stage=32)
+
+
+def test_ties_and_global_ids():
+    one = _query(120, 6)
+    lens = np.full(300, 120)
+    db = random_db(10, lens)
+    for i in range(0, 300, 3):             # many identical subjects -> ties
+        db.residues[db.offsets[i]:db.offsets[i] + 120] = one
+    gids = np.random.default_rng(0).permutation(10_000)[:300].astype(np.int64) * 7
+    _check(db, _query(100, 7), B62, 2, 12, k=37, gids=gids)
+    _check(db, one, B62, 2, 12, k=50, gids=gids)
+
+
+def test_k_larger_than_n_and_tiny_dbs():
+    db = random_db(11, [5, 0, 17])
+    r = _check(db, _query(40, 8), B62, 2, 12, k=6)
+    assert r.topk_ids[3:].tolist() == [-1, -1, -1]
+    _check(random_db(12, [0]), _query(3, 9), B62, 2, 12, k=1)
+    _check(random_db(13, [1]), _query(1, 9), B62, 2, 12, k=1)
+
+
+def test_large_k_uses_full_sort_path():
+    rng = np.random.default_rng(5)
+    db = random_db(14, rng.integers(1, 100, size=6000))
+    _check(db, _query(50, 10), B62, 2, 12, k=5000)
+
+
+def _seq_with_self_score(target, M24):
+    """A sequence of standard residues whose diagonal sum is exactly `target`
+    (closed form: self-score = sum of diagonal under row dominance, reading R13)."""
+    import itertools
+    diag = {int(M24[c, c]): c for c in range(20)}
+    w = max(diag)
+    out = []
+    t = target
+    while t > 4 * w:
+        out.append(diag[w])
+        t -= w
+    for n in range(1, 6):
+        for combo in itertools.combinations_with_replacement(sorted(diag), n):
+            if sum(combo) == t:
+                return np.array(out + [diag[v] for v in combo], dtype=np.uint8)
+    raise AssertionError(t)
+
+
+def test_int16_saturation_limits_exact():
+    """Planted exact copies whose self-score sits at LIMIT16-1, LIMIT16, LIMIT16+1
+    (LIMIT16 = 32767 - s_max): scores stay exact and exactly the subjects above
+    the limit are re-aligned in int32 (DESIGN.md §"Saturation")."""
+    M24 = blosum62()
+    limit = 32767 - 11
+    for target in (limit - 1, limit, limit + 1, 32767, 32768, 40000):
+        q = _seq_with_self_score(target, M24)
+        assert sum(int(M24[c, c]) for c in q) == target
+        lens = np.array([q.size, 50, q.size, 300, 0])
+        db = random_db(15, lens)
+        db.residues[db.offsets[0]:db.offsets[0] + q.size] = q
+        db.residues[db.offsets[2]:db.offsets[2] + q.size] = q[::-1]
+        with sw.Database(db.residues, db.offsets, db.lengths, device=0) as g:
+            res = g.search(q, B62, 2, 12, k=3)
+        ref = oracle.db_scores(q, db, B62, 2, 12)
+        assert ref[0] == target
+        assert np.array_equal(res.scores, ref), (target, res.scores, ref)
+        assert res.stats["n_rerun32"] == int((ref > limit).sum())
+
+
+def test_s16_style_long_query_reruns():
+    """8,000-residue query vs exact and near copies: self-scores ~42k exceed
+    int16, forcing the int32 rerun (stress case S16)."""
+    q = _query(8000, 11)
+    rng = np.random.default_rng(6)
+    lens = np.concatenate([rng.integers(50, 800, size=300), [8000, 8000, 4000]])
+    db = random_db(16, lens)
+    db.residues[db.offsets[300]:db.offsets[300] + 8000] = q
+    mut = q.copy()
+    pos = rng.choice(8000, size=1600, replace=False)
+    mut[pos] = (mut[pos] + 1 + rng.integers(0, 19, size=pos.size)) % 20
+    db.residues[db.offsets[301]:db.offsets[301] + 8000] = mut
+    db.residues[db.offsets[302]:db.offsets[302] + 4000] = q[2000:6000]
+    r = _check(db, q, B62, 2, 12, k=5)
+    assert r.stats["n_rerun32"] >= 2
+
+
+def test_async_api_with_torch_stream():
+    import torch
+    rng = np.random.default_rng(8)
+    db = random_db(17, rng.integers(0, 500, size=2000))
+    q = _query(200, 12)
+    ref = oracle.db_scores(q, db, B62, 2, 12)
+    ti, ts = oracle.topk(ref, 10)
+    with sw.Database.from_synth(db, device=0) as g:
+        s = torch.cuda.Stream()
+        d_sc = torch.empty(db.n_seqs, dtype=torch.int32, device="cuda")
+        d_ti = torch.empty(10, dtype=torch.int64, device="cuda")
+        d_ts = torch.empty(10, dtype=torch.int32, device="cuda")
+        for _ in range(2):      # back-to-back searches on one handle serialise
+            g.search_async(q, B62, 2, 12, 10, d_sc, d_ti, d_ts, stream=s)
+        s.synchronize()
+    assert np.array_equal(d_sc.cpu().numpy(), ref)
+    assert np.array_equal(d_ti.cpu().numpy(), ti) and np.array_equal(d_ts.cpu().numpy(), ts)
+
+
+def test_search_validation_errors():
+    db = random_db(18, [10, 20])
+    with sw.Database.from_synth(db, device=0) as g:
+        q = _query(10, 13)
+        for args, code in [((q, B62, 3, 2, 5), sw.SW_EINVAL),          # beta < alpha
+                           ((q, B62, 2, 12, 0), sw.SW_EINVAL),         # k < 1
+                           ((np.array([], np.uint8), B62, 2, 12, 5), sw.SW_EINVAL),
+                           ((np.array([1, 30], np.uint8), B62, 2, 12, 5), sw.SW_EINVAL)]:
+            with pytest.raises(sw.SwError) as ei:
+                g.search(*args[:4], k=args[4])
+            assert ei.value.code == code
+        Mbad = B62.copy()
+        Mbad[30, 1] = 2
+        with pytest.raises(sw.SwError):
+            g.search(q, Mbad, 2, 12, k=2)
+        Mbig = np.zeros((32, 32), np.int8)
+        Mbig[:24, :24] = 127
+        qbig = np.zeros((1 << 31) // 127 + 1, dtype=np.uint8)
+        with pytest.raises(sw.SwError) as ei:
+            g.search(qbig, Mbig, 2, 12, k=2)
+        assert ei.value.code == sw.SW_ERANGE
