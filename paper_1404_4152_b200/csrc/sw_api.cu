@@ -51,7 +51,18 @@ int fail(int code, const char* fmt, ...) {
                   #call, cudaGetErrorString(_e), __FILE__, __LINE__);                     \
   } while (0)
 
-constexpr int kTileRows = 64;        // query rows per register tile (int16x2 and int32 passes)
+constexpr int kTileRows = 48;        // default query rows per register tile (SW_TILE_ROWS overrides: 32/48/64)
+
+int tile_rows_env() {
+  const char* e = getenv("SW_TILE_ROWS");
+  const int v = e ? atoi(e) : kTileRows;
+  return (v == 32 || v == 48 || v == 64) ? v : kTileRows;
+}
+
+template <int T>
+void* inter16_kernel(bool smem) {
+  return smem ? (void*)swk::k_inter16<T, true> : (void*)swk::k_inter16<T, false>;
+}
 constexpr int kMaxSmemProfile = 200 * 1024;
 
 int host_threads() {
@@ -87,6 +98,7 @@ struct sw_db {
   int64_t n_seqs = 0, n_residues = 0, n_inter = 0, n_intra = 0, sum_len = 0;
   int32_t max_len = 0, max_inter_len = 0;
   int64_t n_groups = 0, n_words = 0;
+  std::vector<int> group_ncols;   // host copy (ascending): picks the intra-task groups per search
 
   uint2* d_words = nullptr;
   GroupDesc* d_groups = nullptr;
@@ -129,6 +141,7 @@ struct sw_db {
   cudaEvent_t ev_ring[kRing][5] = {};
   int64_t n_searches = 0;
   int64_t launches = 0;           // kernels launched by this handle (all searches)
+  int last_n_long = 0;            // groups aligned pair-wise by the intra-task path in the last search
 };
 
 extern "C" {
@@ -261,14 +274,11 @@ static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_
   std::vector<int> len_sorted(n_seqs);
   for (int64_t p = 0; p < n_seqs; p++) len_sorted[p] = lengths[perm[p]];
 
-  // ---- inter/intra split (the intra-task kernel takes subjects > threshold) ----
+  // ---- one layout for both kernels: the intra-task path reads long groups pair by pair ----
   db->long_threshold = o->long_threshold;
-  int64_t n_inter = n_seqs;
-  if (db->long_threshold > 0)
-    n_inter = std::upper_bound(len_sorted.begin(), len_sorted.end(), db->long_threshold) - len_sorted.begin();
+  const int64_t n_inter = n_seqs;
   db->n_inter = n_inter;
-  db->n_intra = n_seqs - n_inter;
-  if (db->n_intra > 0) return fail(SW_EINVAL, "long_threshold: intra-task kernel not available in this build");
+  db->n_intra = 0;
   db->max_inter_len = n_inter ? len_sorted[n_inter - 1] : 0;
 
   // ---- groups of 64 consecutive sorted subjects, 5-bit codes, 6 per word ----
@@ -285,6 +295,8 @@ static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_
   }
   db->n_groups = n_groups;
   db->n_words = base;
+  db->group_ncols.resize(n_groups);
+  for (int64_t g = 0; g < n_groups; g++) db->group_ncols[g] = groups[g].ncols;
 
   CK(cudaMalloc(&db->d_words, std::max<int64_t>(base, 1) * sizeof(uint2)));
   {
@@ -401,7 +413,6 @@ int sw_db_create(const uint8_t* residues, int64_t n_residues, const int64_t* off
   if (o.first_stage != 8 && o.first_stage != 16 && o.first_stage != 32)
     return fail(SW_EINVAL, "first_stage must be 8, 16 or 32 (got %d)", o.first_stage);
   if (o.first_stage == 8) return fail(SW_EINVAL, "first_stage 8: int8 stage not available in this build");
-  if (o.long_threshold == 0) o.long_threshold = -1;   // default: all subjects inter-task (this build)
   {
     int rc = validate_db(residues, n_residues, offsets, lengths, n_seqs, global_ids);
     if (rc != SW_OK) return rc;
@@ -515,15 +526,33 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   const size_t smem_bytes = smem ? prof_bytes : 0;
   const int grid = db->num_sms;   // one persistent 384-thread CTA per SM
   const int limit16 = 32767 - smax;
+  // groups whose inter-task work would exceed ~1/3 of a warp's average share are
+  // split into pairs for the intra-task wavefront (load balance; DESIGN.md §"Work queue")
+  int n_long = 0;
+  {
+    int64_t cut = 0;   // groups with ncols > cut go intra
+    const int64_t n_warps = (int64_t)db->num_sms * (swk::kInterThreads / 32);
+    if (db->long_threshold > 0) cut = db->long_threshold;
+    else if (db->long_threshold == 0) cut = std::max<int64_t>(256, db->sum_len / (64 * std::max<int64_t>(n_warps, 1)));
+    else cut = INT64_MAX;
+    if (const char* e = getenv("SW_LONG_COLS")) cut = atoll(e);
+    const auto it = std::upper_bound(db->group_ncols.begin(), db->group_ncols.end(), (int)std::min<int64_t>(cut, INT32_MAX));
+    n_long = (int)(db->group_ncols.end() - it);
+  }
+  db->last_n_long = n_long;
   if (db->n_inter > 0) {
     if (db->first_stage == 16) {
-      auto kern = smem ? swk::k_inter16<kTileRows, true> : swk::k_inter16<kTileRows, false>;
+      const int T = tile_rows_env();
+      void* kern = T == 32 ? inter16_kernel<32>(smem) : T == 48 ? inter16_kernel<48>(smem) : inter16_kernel<64>(smem);
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
-      kern<<<grid, swk::kInterThreads, smem_bytes, st>>>(
-          db->d_words, db->d_groups, (int)db->n_groups, db->d_prof, m_pad, stride, alpha, beta, limit16,
-          db->d_scratch, db->scratch_cols, db->d_counters + 0, db->d_score_sorted, db->d_counters + 1,
-          db->d_flags);
-      CK(cudaGetLastError());
+      int n_groups_i = (int)db->n_groups;
+      long long scols = db->scratch_cols;
+      int* ctr0 = db->d_counters + 0;
+      int* ctr1 = db->d_counters + 1;
+      void* kargs[] = {&db->d_words, &db->d_groups, &n_groups_i, &n_long, &db->d_prof, (void*)&m_pad, (void*)&stride,
+                       &alpha, &beta, (void*)&limit16, &db->d_scratch, &scols, &ctr0, &db->d_score_sorted,
+                       &ctr1, &db->d_flags};
+      CK(cudaLaunchKernel(kern, dim3(grid), dim3(swk::kInterThreads), kargs, smem_bytes, st));
       nl++;
     }
     CK(cudaEventRecord(ev[2], st));
@@ -657,8 +686,15 @@ int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matri
     memset(stats, 0, sizeof *stats);
     stats->cells = (int64_t)qlen * db->sum_len;
     stats->n_seqs = db->n_seqs;
-    stats->n_inter = db->n_inter;
-    stats->n_intra = db->n_intra;
+    {
+      int64_t n_intra = 0;
+      for (int t = 0; t < db->last_n_long; t++) {
+        const int64_t g = db->n_groups - 1 - t;
+        n_intra += std::min<int64_t>(swk::kGroup, db->n_inter - g * swk::kGroup);
+      }
+      stats->n_intra = n_intra;
+      stats->n_inter = db->n_inter - n_intra;
+    }
     stats->n_rerun32 = db->first_stage == 16 ? counters[1] : 0;
     stats->seconds = std::chrono::duration<double>(t1 - t0).count();
     stats->gcups = stats->seconds > 0 ? (double)stats->cells / stats->seconds / 1e9 : 0.0;

@@ -71,67 +71,109 @@ __global__ void k_profile(const uint8_t* __restrict__ q, int m, const int8_t* __
 }
 
 // ---------------------------------------------------------------------------
-// int16x2 tile: rows [i0, i0+R) of the query against all columns of one pair
-// of subjects.  Registers: H[r] = H(i0+r, j-1), F[r] = F(i0+r, j); e flows
-// down the rows of the current column.  bnd[j] carries (E(i0,j), H(i0-1,j))
-// in and (E(i0+R,j), H(i0+R-1,j)) out between tiles (the paper's "tiled SW
-// computation").
-// Per row: 2 VIADD.16x2 (fma-side pipe) + VIMNMX3 + 2 VIADDMNMX.RELU + 1/2
-// VIMNMX3 + PRMT (alu pipe) for two cells.
+// One column j of R query rows [i0, i0+R) for a pair of subjects (int16x2).
+//   in : D[r] = H(i0+r-1, j-1) + fsbt(q_{i0+r}, s_j)   (diagonal term, precomputed)
+//        F[r] = F(i0+r, j), e = E(i0, j), htop = H(i0-1, j)
+//        plo/phi -> profile rows of the NEXT column's residues (lo/hi subject)
+//   out: D[r] = H(i0+r-1, j) + fsbt(q_{i0+r}, s_{j+1}), F[r] = F(i0+r, j+1),
+//        e = E(i0+R, j); returns H(i0+R-1, j); hmax folds every H(i, j).
+// Per row (two cells): VIMNMX3 + 2 VIADDMNMX.RELU + 1/2 VIMNMX3 + PRMT on the
+// alu pipe, 2 VIADD.16x2 on the fma-side pipe (DESIGN.md §"Cell update").
+// The diagonal add is done one column ahead so ptxas cannot fuse it into an
+// alu-pipe VIADDMNMX, and D is updated in place (no register moves).
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ uint32_t col16(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t& e, uint32_t htop,
+                                          const int8_t* __restrict__ plo, const int8_t* __restrict__ phi,
+                                          uint32_t na2, uint32_t nb2, uint32_t& hmax) {
+  uint32_t hprev = htop, hodd = 0u;
+  uint2 a = *reinterpret_cast<const uint2*>(plo);
+  uint2 b = *reinterpret_cast<const uint2*>(phi);
+#pragma unroll
+  for (int k = 0; k < R / 8; k++) {
+    uint2 an = a, bn = b;
+    if (k + 1 < R / 8) {
+      an = *reinterpret_cast<const uint2*>(plo + 8 * (k + 1));
+      bn = *reinterpret_cast<const uint2*>(phi + 8 * (k + 1));
+    }
+#pragma unroll
+    for (int rr = 0; rr < 8; rr++) {
+      const int r = 8 * k + rr;
+      const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);          // H(i,j) >= 0 since e, F >= 0
+      const uint32_t sn = prmt(rr < 4 ? a.x : a.y, rr < 4 ? b.x : b.y, sel_pair(rr & 3));
+      D[r] = __vadd2(hprev, sn);                                 // H(i-1,j) + fsbt(q_i, s_{j+1}); wraps only past LIMIT16
+      const uint32_t hb = __vadd2(h, nb2);                       // H(i,j) - beta
+      e = __viaddmax_s16x2_relu(e, na2, hb);                     // E(i+1,j)
+      F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);               // F(i,j+1)
+      if (rr & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
+      else hodd = h;
+      hprev = h;
+    }
+    a = an;
+    b = bn;
+  }
+  return hprev;
+}
+
+// Residue cursor over one lane's interleaved packed words (6 codes per word).
+struct ResCursor {
+  uint2 w, wn;
+  int c, wi, nwords;
+  const uint2* base;   // word wi of this lane at base[wi * 32]
+  __device__ __forceinline__ void init(const uint2* b, int nw) {
+    base = b;
+    nwords = nw;
+    c = 0;
+    wi = 0;
+    const uint2 dd = make_uint2(kDummyWord, kDummyWord);
+    w = nw > 0 ? __ldg(b) : dd;
+    wn = nw > 1 ? __ldg(b + 32) : dd;
+  }
+  __device__ __forceinline__ uint32_t lo() const { return (w.x >> (5u * (uint32_t)c)) & 31u; }
+  __device__ __forceinline__ uint32_t hi() const { return (w.y >> (5u * (uint32_t)c)) & 31u; }
+  __device__ __forceinline__ void next() {
+    if (++c == kResPerWord) {
+      c = 0;
+      ++wi;
+      w = wn;
+      const uint2 dd = make_uint2(kDummyWord, kDummyWord);
+      wn = (wi + 1 < nwords) ? __ldg(base + (wi + 1) * 32) : dd;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Inter-task tile: rows [i0, i0+R) of the query against all columns of one
+// pair of subjects per lane (32 pairs = one 64-subject group per warp).
+// bnd[j] carries (E(i0,j), H(i0-1,j)) in and (E(i0+R,j), H(i0+R-1,j)) out
+// between tiles (the paper's "tiled SW computation").
 // ---------------------------------------------------------------------------
 template <int R>
 __device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
                                        const int8_t* __restrict__ prof, int stride, int i0,
                                        uint2* __restrict__ bnd, bool first, bool last,
                                        uint32_t na2, uint32_t nb2, uint32_t& hmax, int lane) {
-  uint32_t H[R], F[R];
-#pragma unroll
-  for (int r = 0; r < R; r++) { H[r] = 0u; F[r] = 0u; }
   if (ncols <= 0) return;
-  const int nwords = (ncols + kResPerWord - 1) / kResPerWord;
-  uint2 res = __ldg(gw + lane);
-  uint2 res_nx = nwords > 1 ? __ldg(gw + 32 + lane) : res;
+  uint32_t D[R], F[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) { D[r] = 0u; F[r] = 0u; }
+  ResCursor rc;
+  rc.init(gw + lane, (ncols + kResPerWord - 1) / kResPerWord);
+  {  // virtual column j = -1 (all-zero boundary): primes D[r] = fsbt(q_{i0+r}, s_0)
+    uint32_t e0 = 0u;
+    col16<R>(D, F, e0, 0u, prof + rc.lo() * stride + i0, prof + rc.hi() * stride + i0, na2, nb2, hmax);
+    rc.next();
+  }
   uint2 bc = first ? make_uint2(0u, 0u) : bnd[lane];
-  uint32_t htop_prev = 0u;   // H(i0-1, j-1)
-  int c = 0, w = 0;
   for (int j = 0; j < ncols; j++) {
     uint2 bn = make_uint2(0u, 0u);
     if (!first && j + 1 < ncols) bn = bnd[(j + 1) * 32 + lane];
-    const uint32_t sh = 5u * (uint32_t)c;
-    const uint32_t rlo = (res.x >> sh) & 31u, rhi = (res.y >> sh) & 31u;
-    const int8_t* plo = prof + rlo * stride + i0;
-    const int8_t* phi = prof + rhi * stride + i0;
-    uint32_t e = bc.x;          // E(i0, j)
-    uint32_t diag = htop_prev;  // H(i0-1, j-1)
-    htop_prev = bc.y;
-    uint32_t hodd = 0u;
-#pragma unroll
-    for (int k = 0; k < R / 8; k++) {
-      const uint2 a = *reinterpret_cast<const uint2*>(plo + 8 * k);
-      const uint2 b = *reinterpret_cast<const uint2*>(phi + 8 * k);
-#pragma unroll
-      for (int rr = 0; rr < 8; rr++) {
-        const int r = 8 * k + rr;
-        const uint32_t s = prmt(rr < 4 ? a.x : a.y, rr < 4 ? b.x : b.y, sel_pair(rr & 3));
-        const uint32_t ds = __vadd2(diag, s);              // H(i-1,j-1) + fsbt (wraps only past LIMIT16)
-        const uint32_t h = __vimax3_s16x2(ds, e, F[r]);    // H(i,j) >= 0 since e, F >= 0
-        diag = H[r];
-        H[r] = h;
-        const uint32_t hb = __vadd2(h, nb2);               // H(i,j) - beta
-        e = __viaddmax_s16x2_relu(e, na2, hb);             // E(i+1,j)
-        F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);       // F(i,j+1)
-        if (rr & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
-        else hodd = h;
-      }
-    }
-    if (!last) bnd[j * 32 + lane] = make_uint2(e, H[R - 1]);
+    uint32_t e = bc.x;                                            // E(i0, j)
+    const uint32_t hl = col16<R>(D, F, e, bc.y, prof + rc.lo() * stride + i0,
+                                 prof + rc.hi() * stride + i0, na2, nb2, hmax);
+    if (!last) bnd[j * 32 + lane] = make_uint2(e, hl);
     bc = bn;
-    if (++c == kResPerWord) {
-      c = 0;
-      ++w;
-      res = res_nx;
-      if (w + 1 < nwords) res_nx = __ldg(gw + (w + 1) * 32 + lane);
-    }
+    rc.next();
   }
 }
 
@@ -145,6 +187,69 @@ __device__ __forceinline__ void tile16_rem(int rem, const uint2* gw, int ncols, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Intra-task wavefront for ONE pair of long subjects per warp (north star (c);
+// the role of the paper's intra-sequence model, with a
+// wavefront instead of Farrar striping).  Lane l owns query rows
+// [base + l*TR, base + (l+1)*TR) of a pass of 32*TR rows and processes column
+// j = s - l at step s; (E, H, next residue) flow to lane l+1 by SHFL.  The
+// last active lane's output row is kept in gbnd for the next pass.
+// Returns this lane's running max (to be reduced over the warp).
+// ---------------------------------------------------------------------------
+template <int TR>
+__device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, int ncols,
+                                                 const int8_t* __restrict__ prof, int stride, int m_pad,
+                                                 uint2* __restrict__ gbnd, long long gstride,
+                                                 uint32_t na2, uint32_t nb2, int lane) {
+  uint32_t hmax = 0u;
+  const int nwords = (ncols + kResPerWord - 1) / kResPerWord;
+  int pass = 0;
+  for (int base = 0; base < m_pad; base += 32 * TR, pass++) {
+    const int nact = min(32, (m_pad - base + TR - 1) / TR);
+    const bool first = base == 0, last = base + 32 * TR >= m_pad;
+    const uint2* gin = gbnd + (long long)(pass & 1) * gstride;          // written by the previous pass
+    uint2* gout = gbnd + (long long)((pass + 1) & 1) * gstride;
+    const int i0 = base + lane * TR;
+    uint32_t D[TR], F[TR];
+#pragma unroll
+    for (int r = 0; r < TR; r++) { D[r] = 0u; F[r] = 0u; }
+    uint32_t e_out = 0u, h_out = 0u, r_out = 0u;
+    // lane 0's cursor over the pair's residues (uncoalesced single-lane reads)
+    ResCursor rc;
+    rc.init(pw, nwords);
+    uint2 gnext = make_uint2(0u, 0u);
+    if (!first && lane == 0) gnext = gin[0];
+    __syncwarp();
+    for (int s = -1; s < ncols + nact - 1; s++) {
+      uint32_t e_in = __shfl_up_sync(0xffffffffu, e_out, 1);
+      uint32_t h_in = __shfl_up_sync(0xffffffffu, h_out, 1);
+      uint32_t r_in = __shfl_up_sync(0xffffffffu, r_out, 1);
+      const int j = s - lane;
+      if (lane == 0) {
+        r_in = rc.lo() | (rc.hi() << 5);                             // residues of column j+1
+        rc.next();
+        if (first || j < 0) { e_in = 0u; h_in = 0u; }
+        else {
+          e_in = gnext.x;
+          h_in = gnext.y;
+          gnext = (j + 1 < ncols) ? gin[j + 1] : make_uint2(0u, 0u);
+        }
+      }
+      if (lane < nact && j >= -1 && j < ncols) {
+        uint32_t e = e_in;
+        const uint32_t hl = col16<TR>(D, F, e, h_in, prof + (r_in & 31u) * stride + i0,
+                                      prof + (r_in >> 5) * stride + i0, na2, nb2, hmax);
+        e_out = e;
+        h_out = hl;
+        r_out = r_in;
+        if (!last && lane == nact - 1 && j >= 0) gout[j] = make_uint2(e, hl);
+      }
+    }
+    __syncwarp();
+  }
+  return hmax;
+}
+
 __device__ __forceinline__ void load_profile_smem(int8_t* sprof, const int8_t* __restrict__ gprof,
                                                   int stride) {
   const int n16 = (kProfRows * stride + 15) / 16;   // buffers are padded to 16 B
@@ -154,13 +259,32 @@ __device__ __forceinline__ void load_profile_smem(int8_t* sprof, const int8_t* _
   __syncthreads();
 }
 
-// (ii) inter-task first pass, int16x2.  Persistent: one CTA per SM, each warp
-// pulls 64-subject groups longest-first from an atomic counter (the device
-// analogue of the paper's guided OpenMP schedule over length-sorted sequence
-// profiles).
+// (ii) first pass, int16x2.  Persistent: one CTA per SM; each warp pulls work
+// items longest-first from an atomic counter (the device analogue of the
+// paper's guided OpenMP schedule over length-sorted sequence profiles,
+// PAPER.md:63-65, 73).  Items [0, 32*n_long) are single PAIRS of the n_long
+// longest groups, aligned by the intra-task wavefront; the rest are whole
+// 64-subject groups, aligned inter-task (one pair per lane).
+__device__ __forceinline__ void emit_pair(uint32_t hmax, int g, int slot, int count, int limit,
+                                          int* __restrict__ score_sorted, int* __restrict__ flag_count,
+                                          int* __restrict__ flag_list) {
+  const int pos = g * kGroup + slot;
+  const int lo = (int)(int16_t)(hmax & 0xffffu), hi = (int)(int16_t)(hmax >> 16);
+  if (slot < count) {
+    score_sorted[pos] = lo;
+    if (lo > limit || lo < 0) flag_list[atomicAdd(flag_count, 1)] = pos;
+  }
+  if (slot + 1 < count) {
+    score_sorted[pos + 1] = hi;
+    if (hi > limit || hi < 0) flag_list[atomicAdd(flag_count, 1)] = pos + 1;
+  }
+}
+
+constexpr int kIntraRows = 16;   // rows per lane in the intra-task wavefront
+
 template <int T, bool SMEM>
 __global__ void __launch_bounds__(kInterThreads, 1)
-k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
+k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups, int n_long,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
           int* __restrict__ score_sorted, int* __restrict__ flag_count, int* __restrict__ flag_list) {
@@ -175,12 +299,26 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   uint2* bnd = scratch + wslot * scratch_cols * 32;
   const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
   const int nfull = m_pad / T, rem = m_pad - nfull * T;
+  const int n_long_items = n_long * 32;
+  const int n_items = n_long_items + (n_groups - n_long);
   for (;;) {
-    int gi = 0;
-    if (lane == 0) gi = atomicAdd(counter, 1);
-    gi = __shfl_sync(0xffffffffu, gi, 0);
-    if (gi >= n_groups) break;
-    const int g = n_groups - 1 - gi;   // groups are stored shortest-first
+    int item = 0;
+    if (lane == 0) item = atomicAdd(counter, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    if (item < n_long_items) {
+      const int g = n_groups - 1 - item / 32;
+      const int p = 31 - item % 32;
+      const GroupDesc gd = groups[g];
+      if (2 * p >= gd.count) continue;
+      uint32_t hm = intra_pair16<kIntraRows>(words + gd.base + p, gd.ncols, prof, stride, m_pad, bnd,
+                                             scratch_cols * 16, na2, nb2, lane);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) hm = __vmaxs2(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+      if (lane == 0) emit_pair(hm, g, 2 * p, gd.count, limit, score_sorted, flag_count, flag_list);
+      continue;
+    }
+    const int g = (n_groups - n_long) - 1 - (item - n_long_items);
     const GroupDesc gd = groups[g];
     const uint2* gw = words + gd.base;
     uint32_t hmax = 0u;
@@ -188,17 +326,7 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
       tile16<T>(gw, gd.ncols, prof, stride, t * T, bnd, t == 0, t == nfull - 1 && rem == 0,
                 na2, nb2, hmax, lane);
     if (rem) tile16_rem<T>(rem, gw, gd.ncols, prof, stride, nfull * T, bnd, nfull == 0, na2, nb2, hmax, lane);
-    const int slot = 2 * lane;
-    const int pos = g * kGroup + slot;
-    const int lo = (int)(int16_t)(hmax & 0xffffu), hi = (int)(int16_t)(hmax >> 16);
-    if (slot < gd.count) {
-      score_sorted[pos] = lo;
-      if (lo > limit || lo < 0) flag_list[atomicAdd(flag_count, 1)] = pos;
-    }
-    if (slot + 1 < gd.count) {
-      score_sorted[pos + 1] = hi;
-      if (hi > limit || hi < 0) flag_list[atomicAdd(flag_count, 1)] = pos + 1;
-    }
+    emit_pair(hmax, g, 2 * lane, gd.count, limit, score_sorted, flag_count, flag_list);
   }
 }
 

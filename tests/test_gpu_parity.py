@@ -43,10 +43,21 @@ def test_lengths_0_to_300_exhaustive():
 
 
 @pytest.mark.parametrize("m", [127, 128, 129, 191, 200, 464, 1000])
-def test_query_tiles_and_ragged_tail(m):
+@pytest.mark.parametrize("long_threshold", [-1, 0, 64])
+def test_query_tiles_and_ragged_tail(m, long_threshold):
+    """long_threshold -1: all inter-task; 0: auto; 64: every group longer than 64
+    columns goes pair-wise through the intra-task wavefront (multi-pass for m > 512)."""
     rng = np.random.default_rng(m)
     lens = np.concatenate([rng.integers(0, 700, size=900), [5, 6, 7, 11, 12, 13, 1, 0]])
-    _check(random_db(m, lens), _query(m, 1), B62, 2, 12)
+    _check(random_db(m, lens), _query(m, 1), B62, 2, 12, long_threshold=long_threshold)
+
+
+@pytest.mark.parametrize("m", [1, 9, 16, 17, 511, 512, 513, 1100])
+def test_intra_wavefront_pass_boundaries(m):
+    """Intra-task path: 16 rows per lane, 512 rows per pass; lane/pass edges."""
+    rng = np.random.default_rng(1000 + m)
+    lens = np.concatenate([rng.integers(100, 1500, size=150), [1, 2, 33]])
+    _check(random_db(2000 + m, lens), _query(m, 2), B62, 2, 12, long_threshold=1)
 
 
 @pytest.mark.parametrize("alpha,beta", [(0, 0), (1, 1), (2, 12), (1, 12), (5, 40), (0, 30), (3, 32767)])
@@ -70,6 +81,15 @@ def test_first_stage_32_equals_oracle():
     rng = np.random.default_rng(4)
     db = random_db(9, rng.integers(0, 600, size=800))
     _check(db, _query(333, 5), B62, 2, 12, first_stage=32)
+
+
+@pytest.mark.parametrize("tile_rows", ["32", "48", "64"])
+def test_tile_rows_invariance(tile_rows, monkeypatch):
+    """Scores do not depend on the register-tile height (T-invariance)."""
+    monkeypatch.setenv("SW_TILE_ROWS", tile_rows)
+    rng = np.random.default_rng(44)
+    db = random_db(19, rng.integers(0, 900, size=1500))
+    _check(db, _query(377, 15), B62, 2, 12, long_threshold=-1)
 
 
 def test_ties_and_global_ids():
@@ -150,7 +170,9 @@ def test_s16_style_long_query_reruns():
     db.residues[db.offsets[301]:db.offsets[301] + 8000] = mut
     db.residues[db.offsets[302]:db.offsets[302] + 4000] = q[2000:6000]
     r = _check(db, q, B62, 2, 12, k=5)
-    assert r.stats["n_rerun32"] >= 2
+    _check(db, q, B62, 2, 12, k=5, long_threshold=1000)     # long copies via the intra path
+    ref = oracle.db_scores(q, db, B62, 2, 12)
+    assert ref[300] > 40000 and r.stats["n_rerun32"] == int((ref > 32767 - 11).sum()) >= 1
 
 
 def test_async_api_with_torch_stream():
