@@ -59,9 +59,20 @@ int tile_rows_env() {
   return (v == 32 || v == 48 || v == 64) ? v : kTileRows;
 }
 
-template <int T>
+int threads_env(int def) {
+  const char* e = getenv("SW_THREADS");
+  const int v = e ? atoi(e) : def;
+  return (v == 256 || v == 384 || v == 512) ? v : def;
+}
+
+template <int T, int NT>
 void* inter16_kernel(bool smem) {
-  return smem ? (void*)swk::k_inter16<T, true> : (void*)swk::k_inter16<T, false>;
+  return smem ? (void*)swk::k_inter16<T, true, NT> : (void*)swk::k_inter16<T, false, NT>;
+}
+
+template <int T>
+void* inter16_kernel_nt(bool smem, int nt) {
+  return nt == 512 ? inter16_kernel<T, 512>(smem) : nt == 256 ? inter16_kernel<T, 256>(smem) : inter16_kernel<T, 384>(smem);
 }
 constexpr int kMaxSmemProfile = 200 * 1024;
 
@@ -380,7 +391,7 @@ static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_
   }
 
   // ---- DP boundary scratch: one slab per resident warp of the persistent kernels ----
-  db->scratch_slots = db->num_sms * (swk::kInterThreads / 32);
+  db->scratch_slots = db->num_sms * (swk::kMaxThreads / 32);
   db->scratch_cols = ((int64_t)db->max_inter_len + swk::kResPerWord) / swk::kResPerWord * swk::kResPerWord + swk::kResPerWord;
   CK(cudaMalloc(&db->d_scratch, (size_t)db->scratch_slots * db->scratch_cols * 32 * sizeof(uint2)));
 
@@ -543,7 +554,8 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   if (db->n_inter > 0) {
     if (db->first_stage == 16) {
       const int T = tile_rows_env();
-      void* kern = T == 32 ? inter16_kernel<32>(smem) : T == 48 ? inter16_kernel<48>(smem) : inter16_kernel<64>(smem);
+      const int nt = threads_env(T == 32 ? 512 : 384);
+      void* kern = T == 32 ? inter16_kernel_nt<32>(smem, nt) : T == 48 ? inter16_kernel_nt<48>(smem, nt) : inter16_kernel_nt<64>(smem, nt);
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
       int n_groups_i = (int)db->n_groups;
       long long scols = db->scratch_cols;
@@ -552,7 +564,7 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
       void* kargs[] = {&db->d_words, &db->d_groups, &n_groups_i, &n_long, &db->d_prof, (void*)&m_pad, (void*)&stride,
                        &alpha, &beta, (void*)&limit16, &db->d_scratch, &scols, &ctr0, &db->d_score_sorted,
                        &ctr1, &db->d_flags};
-      CK(cudaLaunchKernel(kern, dim3(grid), dim3(swk::kInterThreads), kargs, smem_bytes, st));
+      CK(cudaLaunchKernel(kern, dim3(grid), dim3(nt), kargs, smem_bytes, st));
       nl++;
     }
     CK(cudaEventRecord(ev[2], st));

@@ -25,7 +25,8 @@ constexpr int kDummy = 24;           // padding code, scores 0
 constexpr int kNumCodes = 24;        // real residue codes 0..23
 constexpr int kProfRows = 25;        // profile rows: codes 0..23 + DUMMY
 constexpr uint32_t kDummyWord = 24u | (24u << 5) | (24u << 10) | (24u << 15) | (24u << 20) | (24u << 25);
-constexpr int kInterThreads = 384;   // 12 warps, one persistent CTA per SM
+constexpr int kInterThreads = 384;   // 12 warps, one persistent CTA per SM (default)
+constexpr int kMaxThreads = 512;     // scratch is sized for up to 16 resident warps per SM
 
 struct GroupDesc {
   long long base;   // first uint2 of the group in the packed word array
@@ -80,7 +81,8 @@ __global__ void k_profile(const uint8_t* __restrict__ q, int m, const int8_t* __
 // Per row (two cells): VIMNMX3 + 2 VIADDMNMX.RELU + 1/2 VIMNMX3 + PRMT on the
 // alu pipe, 2 VIADD.16x2 on the fma-side pipe (DESIGN.md §"Cell update").
 // The diagonal add is done one column ahead so ptxas cannot fuse it into an
-// alu-pipe VIADDMNMX, and D is updated in place (no register moves).
+// alu-pipe VIADDMNMX, and D is updated in place (no register moves).  (Taking
+// E - alpha off the E chain costs a third VIADD.16x2 and measured 3% slower.)
 // ---------------------------------------------------------------------------
 template <int R>
 __device__ __forceinline__ uint32_t col16(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t& e, uint32_t htop,
@@ -103,8 +105,8 @@ __device__ __forceinline__ uint32_t col16(uint32_t (&D)[R], uint32_t (&F)[R], ui
       const uint32_t sn = prmt(rr < 4 ? a.x : a.y, rr < 4 ? b.x : b.y, sel_pair(rr & 3));
       D[r] = __vadd2(hprev, sn);                                 // H(i-1,j) + fsbt(q_i, s_{j+1}); wraps only past LIMIT16
       const uint32_t hb = __vadd2(h, nb2);                       // H(i,j) - beta
-      e = __viaddmax_s16x2_relu(e, na2, hb);                     // E(i+1,j)
-      F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);               // F(i,j+1)
+      e = __viaddmax_s16x2_relu(e, na2, hb);                     // E(i+1,j) = max(E - alpha, H - beta, 0)
+      F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);               // F(i,j+1) = max(F - alpha, H - beta, 0)
       if (rr & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
       else hodd = h;
       hprev = h;
@@ -164,15 +166,18 @@ __device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
     col16<R>(D, F, e0, 0u, prof + rc.lo() * stride + i0, prof + rc.hi() * stride + i0, na2, nb2, hmax);
     rc.next();
   }
-  uint2 bc = first ? make_uint2(0u, 0u) : bnd[lane];
+  const uint2 z = make_uint2(0u, 0u);
+  uint2 bc = first ? z : bnd[lane];
+  uint2 b1 = (first || ncols < 2) ? z : bnd[32 + lane];
   for (int j = 0; j < ncols; j++) {
-    uint2 bn = make_uint2(0u, 0u);
-    if (!first && j + 1 < ncols) bn = bnd[(j + 1) * 32 + lane];
+    uint2 b2 = z;                                                 // prefetch two columns ahead
+    if (!first && j + 2 < ncols) b2 = bnd[(j + 2) * 32 + lane];
     uint32_t e = bc.x;                                            // E(i0, j)
     const uint32_t hl = col16<R>(D, F, e, bc.y, prof + rc.lo() * stride + i0,
                                  prof + rc.hi() * stride + i0, na2, nb2, hmax);
     if (!last) bnd[j * 32 + lane] = make_uint2(e, hl);
-    bc = bn;
+    bc = b1;
+    b1 = b2;
     rc.next();
   }
 }
@@ -282,8 +287,8 @@ __device__ __forceinline__ void emit_pair(uint32_t hmax, int g, int slot, int co
 
 constexpr int kIntraRows = 16;   // rows per lane in the intra-task wavefront
 
-template <int T, bool SMEM>
-__global__ void __launch_bounds__(kInterThreads, 1)
+template <int T, bool SMEM, int NT>
+__global__ void __launch_bounds__(NT, 1)
 k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups, int n_long,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
