@@ -202,7 +202,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--first-stage", type=int, default=16)
     ap.add_argument("--n-per-rank", type=int, default=None)
-    ap.add_argument("--ref-sample", type=int, default=20000)
+    ap.add_argument("--ref-sample", type=int, default=100000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
