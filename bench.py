@@ -184,11 +184,13 @@ def cpu_baseline(base, q, db, seconds_target=12.0):
 
 
 def load_ncu_traffic():
-    path = os.path.join(ROOT, "profiles", "ncu_inter16_summary.json")
+    """DRAM bytes per k_inter16 launch from the newest committed ncu --set full summary."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_inter16*.json")))
     try:
-        with open(path) as f:
+        with open(paths[-1]) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch")
+        return {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"), "source": os.path.relpath(paths[-1], ROOT)}
     except Exception:
         return None
 
