@@ -166,19 +166,29 @@ __device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
     col16<R>(D, F, e0, 0u, prof + rc.lo() * stride + i0, prof + rc.hi() * stride + i0, na2, nb2, hmax);
     rc.next();
   }
+  // Two columns per iteration: the boundary row of column j is loaded two columns
+  // ahead into the register it is consumed from (bE for even, bO for odd j), so
+  // no register copy waits on an in-flight load.
   const uint2 z = make_uint2(0u, 0u);
-  uint2 bc = first ? z : bnd[lane];
-  uint2 b1 = (first || ncols < 2) ? z : bnd[32 + lane];
-  for (int j = 0; j < ncols; j++) {
-    uint2 b2 = z;                                                 // prefetch two columns ahead
-    if (!first && j + 2 < ncols) b2 = bnd[(j + 2) * 32 + lane];
-    uint32_t e = bc.x;                                            // E(i0, j)
-    const uint32_t hl = col16<R>(D, F, e, bc.y, prof + rc.lo() * stride + i0,
-                                 prof + rc.hi() * stride + i0, na2, nb2, hmax);
-    if (!last) bnd[j * 32 + lane] = make_uint2(e, hl);
-    bc = b1;
-    b1 = b2;
-    rc.next();
+  uint2 bE = first ? z : bnd[lane];
+  uint2 bO = (first || ncols < 2) ? z : bnd[32 + lane];
+  for (int j = 0; j < ncols; j += 2) {
+    {
+      uint32_t e = bE.x;                                          // E(i0, j)
+      const uint32_t hl = col16<R>(D, F, e, bE.y, prof + rc.lo() * stride + i0,
+                                   prof + rc.hi() * stride + i0, na2, nb2, hmax);
+      if (!first && j + 2 < ncols) bE = bnd[(j + 2) * 32 + lane];
+      if (!last) bnd[j * 32 + lane] = make_uint2(e, hl);
+      rc.next();
+    }
+    if (j + 1 < ncols) {
+      uint32_t e = bO.x;                                          // E(i0, j+1)
+      const uint32_t hl = col16<R>(D, F, e, bO.y, prof + rc.lo() * stride + i0,
+                                   prof + rc.hi() * stride + i0, na2, nb2, hmax);
+      if (!first && j + 3 < ncols) bO = bnd[(j + 3) * 32 + lane];
+      if (!last) bnd[(j + 1) * 32 + lane] = make_uint2(e, hl);
+      rc.next();
+    }
   }
 }
 
