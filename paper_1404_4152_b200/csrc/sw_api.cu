@@ -133,8 +133,18 @@ struct sw_db {
   unsigned long long* d_cand = nullptr;
   unsigned long long* d_cand2 = nullptr;
   int cand_cap = 0;
-  int* d_flags = nullptr;         // flagged sorted positions
-  int* d_counters = nullptr;      // [0] inter work, [1] flag count, [2] rerun work, [3] cand count
+  uint8_t* d_flag8 = nullptr;     // per sorted position: saturated in the int8 pass
+  uint8_t* d_flag16 = nullptr;    // per sorted position: saturated in the int16 pass
+  int* d_list8 = nullptr;         // ascending flagged positions (int8 -> int16)
+  int* d_list16 = nullptr;        // ascending flagged positions (int16 -> int32)
+  int* d_block_counts = nullptr;  // compaction scratch
+  int* d_cnt = nullptr;           // [0] #flagged int8, [1] #flagged int16, [2] #mini-groups
+  int64_t n_mini_max = 0;
+  int* d_mini_sizes = nullptr;    // words per mini-group -> exclusive scan = bases
+  GroupDesc* d_mgroups = nullptr; // mini-group layout of the int8-flagged subjects
+  uint2* d_mwords = nullptr;
+  uint8_t* d_prof8b = nullptr;    // biased uint8 profile of the int8 stage
+  int* d_counters = nullptr;      // work counters: [0] first pass, [2] int32 list, [3] cand count, [4] int16 rerun
   unsigned* d_hist = nullptr;
   swk::SelState* d_sel = nullptr;
   long long* d_topk_ids = nullptr;
@@ -153,6 +163,7 @@ struct sw_db {
   int64_t n_searches = 0;
   int64_t launches = 0;           // kernels launched by this handle (all searches)
   int last_n_long = 0;            // groups aligned pair-wise by the intra-task path in the last search
+  int last_first_stage = 16;      // lane width of the last search's first pass
 };
 
 extern "C" {
@@ -185,7 +196,9 @@ static void free_db(sw_db* db) {
   if (db->stream) cudaStreamSynchronize(db->stream);
   void* ptrs[] = {db->d_words, db->d_groups, db->d_perm, db->d_len_sorted, db->d_gid, db->d_scratch,
                   db->d_query, db->d_matrix, db->d_prof, db->d_score_sorted, db->d_scores, db->d_keys,
-                  db->d_cand, db->d_cand2, db->d_flags, db->d_counters, db->d_hist, db->d_sel,
+                  db->d_cand, db->d_cand2, db->d_flag8, db->d_flag16, db->d_list8, db->d_list16,
+                  db->d_block_counts, db->d_cnt, db->d_mini_sizes, db->d_mgroups, db->d_mwords, db->d_prof8b,
+                  db->d_counters, db->d_hist, db->d_sel,
                   db->d_topk_ids, db->d_topk_scores, db->d_cub};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -400,7 +413,21 @@ static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_
   CK(cudaMalloc(&db->d_score_sorted, n1 * sizeof(int)));
   CK(cudaMalloc(&db->d_scores, n1 * sizeof(int)));
   CK(cudaMalloc(&db->d_keys, n1 * sizeof(unsigned long long)));
-  CK(cudaMalloc(&db->d_flags, n1 * sizeof(int)));
+  CK(cudaMalloc(&db->d_flag8, n1));
+  CK(cudaMalloc(&db->d_flag16, n1));
+  CK(cudaMalloc(&db->d_list8, n1 * sizeof(int)));
+  CK(cudaMalloc(&db->d_list16, n1 * sizeof(int)));
+  CK(cudaMalloc(&db->d_block_counts, (n1 / swk::kScanBlock + 2) * sizeof(int)));
+  CK(cudaMalloc(&db->d_cnt, 4 * sizeof(int)));
+  CK(cudaMemset(db->d_cnt, 0, 4 * sizeof(int)));
+  db->n_mini_max = n1 / swk::kGroup + 1;
+  if (db->first_stage == 8) {
+    // sum over mini-groups of ncols <= 2 max_len + total/64 (sorted members), see DESIGN.md §"int8 stage"
+    const int64_t mini_words = db->n_words + (2 * (int64_t)db->max_len / swk::kResPerWord + 2 + db->n_mini_max) * 32;
+    CK(cudaMalloc(&db->d_mini_sizes, db->n_mini_max * sizeof(int)));
+    CK(cudaMalloc(&db->d_mgroups, db->n_mini_max * sizeof(GroupDesc)));
+    CK(cudaMalloc(&db->d_mwords, mini_words * sizeof(uint2)));
+  }
   CK(cudaMalloc(&db->d_counters, 8 * sizeof(int)));
   CK(cudaMalloc(&db->d_hist, 256 * sizeof(unsigned)));
   CK(cudaMemset(db->d_hist, 0, 256 * sizeof(unsigned)));
@@ -423,7 +450,6 @@ int sw_db_create(const uint8_t* residues, int64_t n_residues, const int64_t* off
   if (opts) o = *opts;
   if (o.first_stage != 8 && o.first_stage != 16 && o.first_stage != 32)
     return fail(SW_EINVAL, "first_stage must be 8, 16 or 32 (got %d)", o.first_stage);
-  if (o.first_stage == 8) return fail(SW_EINVAL, "first_stage 8: int8 stage not available in this build");
   {
     int rc = validate_db(residues, n_residues, offsets, lengths, n_seqs, global_ids);
     if (rc != SW_OK) return rc;
@@ -456,7 +482,7 @@ int sw_db_create(const uint8_t* residues, int64_t n_residues, const int64_t* off
 }
 
 static int validate_search(const sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix,
-                           int32_t alpha, int32_t beta, int32_t k, int* smax_out) {
+                           int32_t alpha, int32_t beta, int32_t k, int* smax_out, int* smin_out) {
   if (!db) return fail(SW_EINVAL, "db is NULL");
   if (!query || !matrix) return fail(SW_EINVAL, "query/matrix must be non-NULL");
   if (qlen < 1) return fail(SW_EINVAL, "qlen must be >= 1 (got %d)", qlen);
@@ -465,16 +491,18 @@ static int validate_search(const sw_db* db, const uint8_t* query, int32_t qlen, 
     return fail(SW_EINVAL, "need 0 <= alpha <= beta <= 32767 (alpha=%d, beta=%d)", alpha, beta);
   for (int i = 0; i < qlen; i++)
     if (query[i] >= SW_NUM_CODES) return fail(SW_EINVAL, "query position %d: residue code %d >= 24", i, query[i]);
-  int smax = 0;
+  int smax = 0, smin = 0;
   for (int r = 0; r < 32; r++)
     for (int c = 0; c < 32; c++) {
       const int v = matrix[r * 32 + c];
       if ((r >= SW_NUM_CODES || c >= SW_NUM_CODES) && v != 0)
         return fail(SW_EINVAL, "matrix[%d][%d] = %d: rows/columns 24..31 must be 0", r, c, v);
       smax = std::max(smax, v);
+      smin = std::min(smin, v);
     }
   if ((int64_t)qlen * smax >= (1LL << 31)) return fail(SW_ERANGE, "qlen * s_max = %lld >= 2^31", (long long)qlen * smax);
   *smax_out = smax;
+  *smin_out = smin;
   return SW_OK;
 }
 
@@ -491,7 +519,7 @@ static int ensure(void** p, size_t* cap, size_t need) {
 // Enqueue the whole search on `st`.  Outputs: d_scores (input order) may be
 // nullptr; top-k always goes to d_tk_ids/d_tk_scores when non-null.
 static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix,
-                          int32_t alpha, int32_t beta, int32_t k, int smax, int* d_scores,
+                          int32_t alpha, int32_t beta, int32_t k, int smax, int smin, int* d_scores,
                           long long* d_tk_ids, int* d_tk_scores, cudaStream_t st) {
   cudaEvent_t* ev = db->ev_ring[db->n_searches % sw_db::kRing];
   int64_t nl = 0;   // kernel launches of this search
@@ -517,9 +545,15 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
     db->query_cap = (int)qcap;
     if (rc) return rc;
     void* dp = db->d_prof;
+    const size_t cap0 = db->prof_cap;
     rc = ensure(&dp, &db->prof_cap, prof_bytes);
     db->d_prof = (int8_t*)dp;
     if (rc) return rc;
+    if (db->first_stage == 8 && (db->prof_cap != cap0 || !db->d_prof8b)) {
+      if (db->d_prof8b) cudaFree(db->d_prof8b);
+      db->d_prof8b = nullptr;
+      CK(cudaMalloc(&db->d_prof8b, db->prof_cap));
+    }
     CK(cudaMemcpyAsync(db->d_matrix, db->h_stage, 1024, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(db->d_query, db->h_stage + 1024, qlen, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(db->ev_stage, st));
@@ -529,6 +563,7 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   swk::k_profile<<<64, 256, 0, st>>>(db->d_query, qlen, db->d_matrix, db->d_prof, stride);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(db->d_counters, 0, 8 * sizeof(int), st));
+  CK(cudaMemsetAsync(db->d_cnt, 0, 4 * sizeof(int), st));
   CK(cudaEventRecord(ev[1], st));
 
   // ---- stage (ii): alignment ----
@@ -551,29 +586,78 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
     n_long = (int)(db->group_ncols.end() - it);
   }
   db->last_n_long = n_long;
+  const int nb_scan = std::max(1, (n + swk::kScanBlock - 1) / swk::kScanBlock);
+  // compaction of a flag byte array into an ascending list of sorted positions
+  auto compact = [&](uint8_t* flag, int* list, int* count, int* tail_groups) -> int {
+    swk::k_flag_count<<<nb_scan, swk::kScanBlock, 0, st>>>(flag, n, db->d_block_counts);
+    swk::k_scan_exclusive<<<1, swk::kScanBlock, 0, st>>>(db->d_block_counts, nb_scan, count, tail_groups);
+    swk::k_flag_scatter<<<nb_scan, swk::kScanBlock, 0, st>>>(flag, n, db->d_block_counts, list);
+    nl += 3;
+    CK(cudaGetLastError());
+    return SW_OK;
+  };
+  const int T = tile_rows_env();
+  const int nt = threads_env(T == 32 ? 512 : 384);
+  void* kern16 = T == 32 ? inter16_kernel_nt<32>(smem, nt) : T == 48 ? inter16_kernel_nt<48>(smem, nt) : inter16_kernel_nt<64>(smem, nt);
+  CK(cudaFuncSetAttribute(kern16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
+  auto launch16 = [&](const uint2* words, const GroupDesc* groups, int n_groups_i, const int* n_groups_dev,
+                      const int* pos_map, int n_long_i, int* counter) -> int {
+    long long scols = db->scratch_cols;
+    void* kargs[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &n_long_i,
+                     &db->d_prof, (void*)&m_pad, (void*)&stride, &alpha, &beta, (void*)&limit16, &db->d_scratch,
+                     &scols, &counter, &db->d_score_sorted, &db->d_flag16};
+    CK(cudaLaunchKernel(kern16, dim3(grid), dim3(nt), kargs, smem_bytes, st));
+    nl++;
+    return SW_OK;
+  };
+  // int8 first stage only when every biased byte fits
+  const int bias = -std::min(0, smin);
+  const bool stage8 = db->first_stage == 8 && beta <= 255 && smax + bias <= 255;
+  db->last_first_stage = db->first_stage == 32 ? 32 : (stage8 ? 8 : 16);
   if (db->n_inter > 0) {
-    if (db->first_stage == 16) {
-      const int T = tile_rows_env();
-      const int nt = threads_env(T == 32 ? 512 : 384);
-      void* kern = T == 32 ? inter16_kernel_nt<32>(smem, nt) : T == 48 ? inter16_kernel_nt<48>(smem, nt) : inter16_kernel_nt<64>(smem, nt);
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
-      int n_groups_i = (int)db->n_groups;
-      long long scols = db->scratch_cols;
-      int* ctr0 = db->d_counters + 0;
-      int* ctr1 = db->d_counters + 1;
-      void* kargs[] = {&db->d_words, &db->d_groups, &n_groups_i, &n_long, &db->d_prof, (void*)&m_pad, (void*)&stride,
-                       &alpha, &beta, (void*)&limit16, &db->d_scratch, &scols, &ctr0, &db->d_score_sorted,
-                       &ctr1, &db->d_flags};
-      CK(cudaLaunchKernel(kern, dim3(grid), dim3(nt), kargs, smem_bytes, st));
-      nl++;
+    if (db->first_stage != 32) CK(cudaMemsetAsync(db->d_flag16, 0, (size_t)n, st));
+    if (stage8) {
+      const int limit8 = 255 - (smax + bias);
+      swk::k_profile8b<<<64, 256, 0, st>>>(db->d_query, qlen, db->d_matrix, bias, db->d_prof8b, stride);
+      CK(cudaMemsetAsync(db->d_flag8, 0, (size_t)n, st));
+      auto k8 = smem ? swk::k_inter8<32, true> : swk::k_inter8<32, false>;
+      CK(cudaFuncSetAttribute(k8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
+      k8<<<grid, swk::kInterThreads, smem_bytes, st>>>(db->d_words, db->d_groups, (int)db->n_groups, db->d_prof8b,
+                                                       m_pad, stride, alpha, beta, bias, limit8, db->d_scratch,
+                                                       db->scratch_cols, db->d_counters + 0, db->d_score_sorted,
+                                                       db->d_flag8);
+      nl += 2;
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(ev[2], st));
+      // escalation 8 -> 16: compact, re-interleave the flagged subjects, int16 pass on the mini layout
+      int rc = compact(db->d_flag8, db->d_list8, db->d_cnt + 0, db->d_cnt + 2);
+      if (rc) return rc;
+      const int nmm = (int)db->n_mini_max;
+      swk::k_mini_sizes<<<std::min((nmm + 255) / 256, 4096), 256, 0, st>>>(db->d_list8, db->d_cnt + 0,
+                                                                          db->d_len_sorted, nmm, db->d_mini_sizes);
+      swk::k_scan_exclusive<<<1, swk::kScanBlock, 0, st>>>(db->d_mini_sizes, nmm, nullptr, nullptr);
+      swk::k_mini_build<<<std::min((nmm + 7) / 8, 8192), 256, 0, st>>>(db->d_words, db->d_groups, db->d_list8,
+                                                                      db->d_cnt + 0, db->d_len_sorted, db->d_mini_sizes,
+                                                                      nmm, db->d_mgroups, db->d_mwords);
+      nl += 3;
+      CK(cudaGetLastError());
+      rc = launch16(db->d_mwords, db->d_mgroups, nmm, db->d_cnt + 2, db->d_list8, 0, db->d_counters + 4);
+      if (rc) return rc;
+    } else if (db->first_stage != 32) {
+      int rc = launch16(db->d_words, db->d_groups, (int)db->n_groups, nullptr, nullptr, n_long, db->d_counters + 0);
+      if (rc) return rc;
+      CK(cudaEventRecord(ev[2], st));
+    } else {
+      CK(cudaEventRecord(ev[2], st));
     }
-    CK(cudaEventRecord(ev[2], st));
     auto k32 = smem ? swk::k_list32<kTileRows, true> : swk::k_list32<kTileRows, false>;
     CK(cudaFuncSetAttribute(k32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
-    if (db->first_stage == 16) {
-      // rerun only the subjects flagged by the int16 pass (count read on device)
+    if (db->first_stage != 32) {
+      // escalation 16 -> 32: rerun only the subjects flagged by the int16 pass (count read on device)
+      int rc = compact(db->d_flag16, db->d_list16, db->d_cnt + 1, nullptr);
+      if (rc) return rc;
       k32<<<grid, swk::kInterThreads, smem_bytes, st>>>(
-          db->d_words, db->d_groups, db->d_flags, db->d_counters + 1, 0, db->d_len_sorted, db->d_prof,
+          db->d_words, db->d_groups, db->d_list16, db->d_cnt + 1, 0, db->d_len_sorted, db->d_prof,
           m_pad, stride, alpha, beta, db->d_scratch, db->scratch_cols, db->d_counters + 2,
           db->d_score_sorted);
     } else {
@@ -601,8 +685,8 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
     if (cnt > 0) {
       const bool take_all = k >= n;
       if (!take_all) {
-        swk::SelState s0{0ull, 0ull, (long long)k};
-        CK(cudaMemcpyAsync(db->d_sel, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+        swk::k_sel_init<<<1, 32, 0, st>>>(db->d_sel, (long long)k);
+        nl++;
         const int hb = std::min((n + 1023) / 1024, db->num_sms * 4);
         for (int shift = 56; shift >= 0; shift -= 8) {
           swk::k_sel_hist<<<hb, 256, 0, st>>>(db->d_keys, n, db->d_sel, shift, db->d_hist);
@@ -651,14 +735,14 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
 int sw_search_async(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix, int32_t alpha,
                     int32_t beta, int32_t k, int32_t* d_scores, int64_t* d_topk_ids,
                     int32_t* d_topk_scores, void* stream) {
-  int smax = 0;
-  int rc = validate_search(db, query, qlen, matrix, alpha, beta, k, &smax);
+  int smax = 0, smin = 0;
+  int rc = validate_search(db, query, qlen, matrix, alpha, beta, k, &smax, &smin);
   if (rc) return rc;
   std::lock_guard<std::mutex> lock(db->mu);
   CK(cudaSetDevice(db->device));
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaStreamWaitEvent(st, db->ev_done, 0));   // serialise with the previous search on this handle
-  return search_enqueue(db, query, qlen, matrix, alpha, beta, k, smax, d_scores, (long long*)d_topk_ids,
+  return search_enqueue(db, query, qlen, matrix, alpha, beta, k, smax, smin, d_scores, (long long*)d_topk_ids,
                         d_topk_scores, st);
 }
 
@@ -666,8 +750,8 @@ int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matri
               int32_t beta, int32_t k, int32_t* scores, int64_t* topk_ids, int32_t* topk_scores,
               sw_stats* stats) {
   const auto t0 = std::chrono::steady_clock::now();
-  int smax = 0;
-  int rc = validate_search(db, query, qlen, matrix, alpha, beta, k, &smax);
+  int smax = 0, smin = 0;
+  int rc = validate_search(db, query, qlen, matrix, alpha, beta, k, &smax, &smin);
   if (rc) return rc;
   std::lock_guard<std::mutex> lock(db->mu);
   CK(cudaSetDevice(db->device));
@@ -683,15 +767,15 @@ int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matri
     }
   }
   cudaStream_t st = db->stream;
-  rc = search_enqueue(db, query, qlen, matrix, alpha, beta, k, smax, db->d_scores, db->d_topk_ids,
+  rc = search_enqueue(db, query, qlen, matrix, alpha, beta, k, smax, smin, db->d_scores, db->d_topk_ids,
                       db->d_topk_scores, st);
   if (rc) return rc;
   if (scores && db->n_seqs)
     CK(cudaMemcpyAsync(scores, db->d_scores, db->n_seqs * sizeof(int), cudaMemcpyDeviceToHost, st));
   if (topk_ids) CK(cudaMemcpyAsync(topk_ids, db->d_topk_ids, (size_t)k * sizeof(long long), cudaMemcpyDeviceToHost, st));
   if (topk_scores) CK(cudaMemcpyAsync(topk_scores, db->d_topk_scores, (size_t)k * sizeof(int), cudaMemcpyDeviceToHost, st));
-  int counters[8] = {0};
-  CK(cudaMemcpyAsync(counters, db->d_counters, sizeof counters, cudaMemcpyDeviceToHost, st));
+  int cnt[4] = {0};
+  CK(cudaMemcpyAsync(cnt, db->d_cnt, sizeof cnt, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const auto t1 = std::chrono::steady_clock::now();
   if (stats) {
@@ -707,7 +791,8 @@ int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matri
       stats->n_intra = n_intra;
       stats->n_inter = db->n_inter - n_intra;
     }
-    stats->n_rerun32 = db->first_stage == 16 ? counters[1] : 0;
+    stats->n_rerun16 = db->last_first_stage == 8 ? cnt[0] : 0;
+    stats->n_rerun32 = db->last_first_stage != 32 ? cnt[1] : 0;
     stats->seconds = std::chrono::duration<double>(t1 - t0).count();
     stats->gcups = stats->seconds > 0 ? (double)stats->cells / stats->seconds / 1e9 : 0.0;
     cudaEvent_t* ev = db->ev_ring[(db->n_searches - 1) % sw_db::kRing];
@@ -716,7 +801,7 @@ int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matri
     cudaEventElapsedTime(&ms, ev[1], ev[2]); stats->ms_inter = ms;
     cudaEventElapsedTime(&ms, ev[2], ev[3]); stats->ms_rerun = ms;
     cudaEventElapsedTime(&ms, ev[3], ev[4]); stats->ms_finalize = ms;
-    stats->first_stage = db->first_stage;
+    stats->first_stage = db->last_first_stage;
   }
   return SW_OK;
 }

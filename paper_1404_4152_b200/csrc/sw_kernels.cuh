@@ -274,24 +274,26 @@ __device__ __forceinline__ void load_profile_smem(int8_t* sprof, const int8_t* _
   __syncthreads();
 }
 
-// (ii) first pass, int16x2.  Persistent: one CTA per SM; each warp pulls work
+// (ii) int16x2 pass (first pass, or the rerun of int8-flagged subjects on a
+// mini-group layout with pos_map).  Persistent: one CTA per SM; each warp pulls work
 // items longest-first from an atomic counter (the device analogue of the
 // paper's guided OpenMP schedule over length-sorted sequence profiles,
 // PAPER.md:63-65, 73).  Items [0, 32*n_long) are single PAIRS of the n_long
 // longest groups, aligned by the intra-task wavefront; the rest are whole
 // 64-subject groups, aligned inter-task (one pair per lane).
 __device__ __forceinline__ void emit_pair(uint32_t hmax, int g, int slot, int count, int limit,
-                                          int* __restrict__ score_sorted, int* __restrict__ flag_count,
-                                          int* __restrict__ flag_list) {
-  const int pos = g * kGroup + slot;
+                                          const int* __restrict__ pos_map, int* __restrict__ score_sorted,
+                                          uint8_t* __restrict__ flag) {
   const int lo = (int)(int16_t)(hmax & 0xffffu), hi = (int)(int16_t)(hmax >> 16);
   if (slot < count) {
+    const int pos = pos_map ? pos_map[g * kGroup + slot] : g * kGroup + slot;
     score_sorted[pos] = lo;
-    if (lo > limit || lo < 0) flag_list[atomicAdd(flag_count, 1)] = pos;
+    if (lo > limit || lo < 0) flag[pos] = 1;
   }
   if (slot + 1 < count) {
-    score_sorted[pos + 1] = hi;
-    if (hi > limit || hi < 0) flag_list[atomicAdd(flag_count, 1)] = pos + 1;
+    const int pos = pos_map ? pos_map[g * kGroup + slot + 1] : g * kGroup + slot + 1;
+    score_sorted[pos] = hi;
+    if (hi > limit || hi < 0) flag[pos] = 1;
   }
 }
 
@@ -299,11 +301,14 @@ constexpr int kIntraRows = 16;   // rows per lane in the intra-task wavefront
 
 template <int T, bool SMEM, int NT>
 __global__ void __launch_bounds__(NT, 1)
-k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups, int n_long,
+k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
+          const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int n_long,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
-          int* __restrict__ score_sorted, int* __restrict__ flag_count, int* __restrict__ flag_list) {
+          int* __restrict__ score_sorted, uint8_t* __restrict__ flag) {
   extern __shared__ __align__(16) int8_t sprof[];
+  if (n_groups_dev) n_groups = *n_groups_dev;   // mini-group layout of a rerun: size known on device only
+  if (n_groups <= 0) return;
   const int8_t* prof = gprof;
   if (SMEM) {
     load_profile_smem(sprof, gprof, stride);
@@ -330,7 +335,7 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
                                              scratch_cols * 16, na2, nb2, lane);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) hm = __vmaxs2(hm, __shfl_xor_sync(0xffffffffu, hm, o));
-      if (lane == 0) emit_pair(hm, g, 2 * p, gd.count, limit, score_sorted, flag_count, flag_list);
+      if (lane == 0) emit_pair(hm, g, 2 * p, gd.count, limit, pos_map, score_sorted, flag);
       continue;
     }
     const int g = (n_groups - n_long) - 1 - (item - n_long_items);
@@ -341,7 +346,171 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
       tile16<T>(gw, gd.ncols, prof, stride, t * T, bnd, t == 0, t == nfull - 1 && rem == 0,
                 na2, nb2, hmax, lane);
     if (rem) tile16_rem<T>(rem, gw, gd.ncols, prof, stride, nfull * T, bnd, nfull == 0, na2, nb2, hmax, lane);
-    emit_pair(hmax, g, 2 * lane, gd.count, limit, score_sorted, flag_count, flag_list);
+    emit_pair(hmax, g, 2 * lane, gd.count, limit, pos_map, score_sorted, flag);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// int8 first stage (biased unsigned bytes): four
+// subjects per lane in the bytes of a 32-bit word (pair `lane` of groups 2u and
+// 2u+1).  H, E, F hold the true (clamped) values in [0, 255]; substitutions are
+// biased by B = -min(0, s_min) so they are unsigned:
+//   H = max(satsub(satadd(H(i-1,j-1), s + B), B), E, F)
+//   E = max(satsub(E, alpha), satsub(H, beta)),  F likewise.
+// Exact until an add saturates, which needs an exactly computed H > LIMIT8 =
+// 255 - (s_max + B); those subjects are flagged and re-aligned at int16.
+// Byte SIMD is emulated on sm_100a (~7-8 instructions per __vaddus4/__vsubus4/
+// __vmaxu4), so this pass is measured, not assumed (DESIGN.md §"int8 stage").
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ uint32_t col8(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t& e, uint32_t htop,
+                                         const uint8_t* __restrict__ p0, const uint8_t* __restrict__ p1,
+                                         const uint8_t* __restrict__ p2, const uint8_t* __restrict__ p3,
+                                         uint32_t a4, uint32_t b4, uint32_t B4, uint32_t& hmax) {
+  uint32_t hprev = htop;
+#pragma unroll
+  for (int k = 0; k < R / 8; k++) {
+    const uint2 q0 = *reinterpret_cast<const uint2*>(p0 + 8 * k);
+    const uint2 q1 = *reinterpret_cast<const uint2*>(p1 + 8 * k);
+    const uint2 q2 = *reinterpret_cast<const uint2*>(p2 + 8 * k);
+    const uint2 q3 = *reinterpret_cast<const uint2*>(p3 + 8 * k);
+#pragma unroll
+    for (int h2 = 0; h2 < 2; h2++) {           // rows 8k + 4*h2 .. +3
+      const uint32_t w0 = h2 ? q0.y : q0.x, w1 = h2 ? q1.y : q1.x;
+      const uint32_t w2 = h2 ? q2.y : q2.x, w3 = h2 ? q3.y : q3.x;
+      // transpose: row t -> (w0.byte t, w1.byte t, w2.byte t, w3.byte t)
+      const uint32_t t01a = prmt(w0, w1, 0x5140u), t23a = prmt(w2, w3, 0x5140u);   // rows 0,1
+      const uint32_t t01b = prmt(w0, w1, 0x7362u), t23b = prmt(w2, w3, 0x7362u);   // rows 2,3
+      uint32_t sv[4];
+      sv[0] = prmt(t01a, t23a, 0x5410u);
+      sv[1] = prmt(t01a, t23a, 0x7632u);
+      sv[2] = prmt(t01b, t23b, 0x5410u);
+      sv[3] = prmt(t01b, t23b, 0x7632u);
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const int r = 8 * k + 4 * h2 + t;
+        const uint32_t h = __vmaxu4(__vmaxu4(__vsubus4(D[r], B4), e), F[r]);
+        D[r] = __vaddus4(hprev, sv[t]);
+        const uint32_t hb = __vsubus4(h, b4);
+        e = __vmaxu4(__vsubus4(e, a4), hb);
+        F[r] = __vmaxu4(__vsubus4(F[r], a4), hb);
+        hmax = __vmaxu4(hmax, h);
+        hprev = h;
+      }
+    }
+  }
+  return hprev;
+}
+
+template <int R>
+__device__ __forceinline__ void tile8(const uint2* __restrict__ gw0, const uint2* __restrict__ gw1, int nw0,
+                                      int nw1, int ncols, const uint8_t* __restrict__ prof, int stride, int i0,
+                                      uint2* __restrict__ bnd, bool first, bool last, uint32_t a4, uint32_t b4,
+                                      uint32_t B4, uint32_t& hmax, int lane) {
+  if (ncols <= 0) return;
+  uint32_t D[R], F[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) { D[r] = 0u; F[r] = 0u; }
+  ResCursor c0, c1;
+  c0.init(gw0 + lane, nw0);
+  c1.init(gw1 + lane, nw1);
+  {
+    uint32_t e0 = 0u;
+    col8<R>(D, F, e0, 0u, prof + c0.lo() * stride + i0, prof + c0.hi() * stride + i0, prof + c1.lo() * stride + i0,
+            prof + c1.hi() * stride + i0, a4, b4, B4, hmax);
+    c0.next();
+    c1.next();
+  }
+  const uint2 z = make_uint2(0u, 0u);
+  uint2 bc = first ? z : bnd[lane];
+  for (int j = 0; j < ncols; j++) {
+    uint2 bn = z;
+    if (!first && j + 1 < ncols) bn = bnd[(j + 1) * 32 + lane];
+    uint32_t e = bc.x;
+    const uint32_t hl = col8<R>(D, F, e, bc.y, prof + c0.lo() * stride + i0, prof + c0.hi() * stride + i0,
+                                prof + c1.lo() * stride + i0, prof + c1.hi() * stride + i0, a4, b4, B4, hmax);
+    if (!last) bnd[j * 32 + lane] = make_uint2(e, hl);
+    bc = bn;
+    c0.next();
+    c1.next();
+  }
+}
+
+template <int T, int R = T - 8>
+__device__ __forceinline__ void tile8_rem(int rem, const uint2* gw0, const uint2* gw1, int nw0, int nw1, int ncols,
+                                          const uint8_t* prof, int stride, int i0, uint2* bnd, bool first,
+                                          uint32_t a4, uint32_t b4, uint32_t B4, uint32_t& hmax, int lane) {
+  if constexpr (R >= 8) {
+    if (rem == R) tile8<R>(gw0, gw1, nw0, nw1, ncols, prof, stride, i0, bnd, first, true, a4, b4, B4, hmax, lane);
+    else tile8_rem<T, R - 8>(rem, gw0, gw1, nw0, nw1, ncols, prof, stride, i0, bnd, first, a4, b4, B4, hmax, lane);
+  }
+}
+
+template <int T, bool SMEM>
+__global__ void __launch_bounds__(kInterThreads, 1)
+k_inter8(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
+         const uint8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int bias, int limit,
+         uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
+         int* __restrict__ score_sorted, uint8_t* __restrict__ flag) {
+  extern __shared__ __align__(16) int8_t sprof[];
+  const uint8_t* prof = gprof;
+  if (SMEM) {
+    load_profile_smem(sprof, reinterpret_cast<const int8_t*>(gprof), stride);
+    prof = reinterpret_cast<const uint8_t*>(sprof);
+  }
+  const int lane = threadIdx.x & 31;
+  const long long wslot = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint2* bnd = scratch + wslot * scratch_cols * 32;
+  const uint32_t a4 = (uint32_t)alpha * 0x01010101u, b4 = (uint32_t)beta * 0x01010101u,
+                 B4 = (uint32_t)bias * 0x01010101u;
+  const int nfull = m_pad / T, rem = m_pad - nfull * T;
+  const int n_units = (n_groups + 1) / 2;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(counter, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_units) break;
+    const int u = n_units - 1 - item;                      // longest first
+    const int g0 = 2 * u, g1 = 2 * u + 1;
+    const GroupDesc d0 = groups[g0];
+    GroupDesc d1;
+    d1.base = 0;
+    d1.ncols = 0;
+    d1.count = 0;
+    if (g1 < n_groups) d1 = groups[g1];
+    const int ncols = max(d0.ncols, d1.ncols);
+    const int nw0 = (d0.ncols + kResPerWord - 1) / kResPerWord, nw1 = (d1.ncols + kResPerWord - 1) / kResPerWord;
+    const uint2* gw0 = words + d0.base;
+    const uint2* gw1 = words + d1.base;
+    uint32_t hmax = 0u;
+    for (int t = 0; t < nfull; t++)
+      tile8<T>(gw0, gw1, nw0, nw1, ncols, prof, stride, t * T, bnd, t == 0, t == nfull - 1 && rem == 0, a4, b4, B4,
+               hmax, lane);
+    if (rem) tile8_rem<T>(rem, gw0, gw1, nw0, nw1, ncols, prof, stride, nfull * T, bnd, nfull == 0, a4, b4, B4, hmax, lane);
+    const int sc[4] = {(int)(hmax & 255u), (int)((hmax >> 8) & 255u), (int)((hmax >> 16) & 255u), (int)(hmax >> 24)};
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      const GroupDesc& d = b < 2 ? d0 : d1;
+      const int g = b < 2 ? g0 : g1;
+      const int slot = 2 * lane + (b & 1);
+      if (slot < d.count) {
+        const int pos = g * kGroup + slot;
+        score_sorted[pos] = sc[b];
+        if (sc[b] > limit) flag[pos] = 1;
+      }
+    }
+  }
+}
+
+// biased uint8 profile for the int8 stage: prof[r][i] = fsbt(q_i, r) + bias (DUMMY/pad: bias)
+__global__ void k_profile8b(const uint8_t* __restrict__ q, int m, const int8_t* __restrict__ M, int bias,
+                            uint8_t* __restrict__ prof, int stride) {
+  const int total = kProfRows * stride;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int r = t / stride, i = t - r * stride;
+    int v = 0;
+    if (i < m && r < kNumCodes) v = M[q[i] * 32 + r];
+    prof[t] = (uint8_t)(v + bias);
   }
 }
 
@@ -460,6 +629,124 @@ k_list32(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
 }
 
 // ---------------------------------------------------------------------------
+// a4 escalation plumbing: deterministic compaction of flagged sorted positions
+// (ascending, hence ascending length) and re-interleaving of the flagged
+// subjects into a mini-group layout for the next, wider pass.
+// ---------------------------------------------------------------------------
+constexpr int kScanBlock = 1024;
+
+__global__ void __launch_bounds__(kScanBlock) k_flag_count(const uint8_t* __restrict__ flag, int n,
+                                                           int* __restrict__ block_counts) {
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  const int f = (i < n && flag[i]) ? 1 : 0;
+  const int c = __syncthreads_count(f);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = c;
+}
+
+// Exclusive scan of `v[0..nb)` in place by one CTA; total -> *total (and, when
+// tail_groups != nullptr, ceil(total/64) -> *tail_groups).
+__global__ void __launch_bounds__(kScanBlock) k_scan_exclusive(int* __restrict__ v, int nb, int* __restrict__ total,
+                                                              int* __restrict__ tail_groups) {
+  __shared__ int sh[kScanBlock];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += kScanBlock) {
+    const int i = base + threadIdx.x;
+    const int x = i < nb ? v[i] : 0;
+    sh[threadIdx.x] = x;
+    __syncthreads();
+    for (int off = 1; off < kScanBlock; off <<= 1) {
+      const int add = threadIdx.x >= off ? sh[threadIdx.x - off] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (i < nb) v[i] = carry + sh[threadIdx.x] - x;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += sh[kScanBlock - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (total) *total = carry;
+    if (tail_groups) *tail_groups = (carry + kGroup - 1) / kGroup;
+  }
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_flag_scatter(const uint8_t* __restrict__ flag, int n,
+                                                             const int* __restrict__ block_offsets,
+                                                             int* __restrict__ list) {
+  __shared__ int warp_sums[kScanBlock / 32];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  const int f = (i < n && flag[i]) ? 1 : 0;
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) warp_sums[w] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < kScanBlock / 32; k++) { const int t = warp_sums[k]; warp_sums[k] = acc; acc += t; }
+  }
+  __syncthreads();
+  if (f) list[block_offsets[blockIdx.x] + warp_sums[w] + __popc(bal & ((1u << lane) - 1u))] = i;
+}
+
+// mini-group sizes (words) of a sorted flagged list: ncols = length of the group's last member
+__global__ void k_mini_sizes(const int* __restrict__ list, const int* __restrict__ count_ptr,
+                             const int* __restrict__ len_sorted, int n_mini_max, int* __restrict__ sizes) {
+  const int cnt = *count_ptr;
+  for (int gm = blockIdx.x * blockDim.x + threadIdx.x; gm < n_mini_max; gm += gridDim.x * blockDim.x) {
+    int words = 0;
+    if (gm * kGroup < cnt) {
+      const int last = min(gm * kGroup + kGroup, cnt) - 1;
+      const int nc = len_sorted[list[last]];
+      words = (nc + kResPerWord - 1) / kResPerWord * 32;
+    }
+    sizes[gm] = words;
+  }
+}
+
+// one warp per mini-group: descriptor + gather of the members' packed words
+__global__ void k_mini_build(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
+                             const int* __restrict__ list, const int* __restrict__ count_ptr,
+                             const int* __restrict__ len_sorted, const int* __restrict__ bases, int n_mini_max,
+                             GroupDesc* __restrict__ mgroups, uint2* __restrict__ mwords) {
+  const int cnt = *count_ptr;
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int gm = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gm < n_mini_max && gm * kGroup < cnt; gm += warps) {
+    const int first = gm * kGroup, count = min(kGroup, cnt - first);
+    const int nc = len_sorted[list[first + count - 1]];
+    const int nw = (nc + kResPerWord - 1) / kResPerWord;
+    if (lane == 0) {
+      GroupDesc d;
+      d.base = bases[gm];
+      d.ncols = nc;
+      d.count = count;
+      mgroups[gm] = d;
+    }
+    const uint32_t* src[2] = {nullptr, nullptr};
+    int own_nw[2] = {0, 0};
+    for (int h = 0; h < 2; h++) {
+      const int slot = 2 * lane + h;
+      if (slot < count) {
+        const int pos = list[first + slot];
+        const int og = pos / kGroup, os = pos % kGroup;
+        src[h] = reinterpret_cast<const uint32_t*>(words) + 2 * (groups[og].base + (os >> 1)) + (os & 1);
+        own_nw[h] = (len_sorted[pos] + kResPerWord - 1) / kResPerWord;
+      }
+    }
+    uint2* dst = mwords + bases[gm] + lane;
+    for (int w = 0; w < nw; w++) {
+      uint2 v;
+      v.x = w < own_nw[0] ? __ldg(src[0] + (long long)w * 64) : kDummyWord;
+      v.y = w < own_nw[1] ? __ldg(src[1] + (long long)w * 64) : kDummyWord;
+      dst[(long long)w * 32] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // (iv) finalize: scatter to input order and build unique 64-bit ranking keys
 // (score << 32 | ~gid): "sort all alignment scores in descending order"
 // (PAPER.md:55), ties by ascending global id (reading R7).
@@ -481,6 +768,14 @@ struct SelState {
   long long kk;     // rank (1-based) still to find inside the current prefix
 };
 
+__global__ void k_sel_init(SelState* st, long long k) {
+  if (threadIdx.x == 0) {
+    st->prefix = 0ull;
+    st->mask = 0ull;
+    st->kk = k;
+  }
+}
+
 // Radix select of the k-th largest key, 8 bits per pass (most significant first).
 __global__ void k_sel_hist(const unsigned long long* __restrict__ keys, int n,
                            const SelState* __restrict__ st, int shift, unsigned* __restrict__ hist) {
@@ -497,20 +792,30 @@ __global__ void k_sel_hist(const unsigned long long* __restrict__ keys, int n,
     if (sh[t]) atomicAdd(&hist[t], sh[t]);
 }
 
-__global__ void k_sel_pick(SelState* st, int shift, unsigned* hist) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    long long kk = st->kk, above = 0;
-    int d = 255;
-    for (; d > 0; d--) {
-      if (above + (long long)hist[d] >= kk) break;
-      above += hist[d];
-    }
-    st->kk = kk - above;
+__global__ void __launch_bounds__(256) k_sel_pick(SelState* st, int shift, unsigned* hist) {
+  // digit d is chosen so that (# keys with digit > d) < kk <= (# keys with digit >= d);
+  // suffix sums over the 256 bins by a block-wide scan (descending digit order)
+  __shared__ long long suf[256];
+  const int t = threadIdx.x;
+  const int d = 255 - t;                       // thread t holds digit 255 - t
+  long long v = hist[d];
+  suf[t] = v;
+  __syncthreads();
+  for (int off = 1; off < 256; off <<= 1) {
+    const long long add = t >= off ? suf[t - off] : 0;
+    __syncthreads();
+    suf[t] += add;
+    __syncthreads();
+  }
+  const long long kk = st->kk;
+  const long long incl = suf[t], excl = incl - v;   // keys with digit >= d, > d
+  __syncthreads();
+  if (excl < kk && kk <= incl) {
+    st->kk = kk - excl;
     st->prefix |= (unsigned long long)d << shift;
     st->mask |= 255ull << shift;
   }
-  __syncthreads();
-  for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0;
+  hist[d] = 0;
 }
 
 __global__ void k_sel_compact(const unsigned long long* __restrict__ keys, int n,

@@ -13,11 +13,11 @@ from swdata.synth import db_lengths
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def _search(cfg, m=None):
+def _search(cfg, m=None, **kw):
     db = make_db(cfg)
     q = make_query(cfg, m)
     M = cfg.matrix32()
-    with sw.Database.from_synth(db, device=0) as g:
+    with sw.Database.from_synth(db, device=0, **kw) as g:
         res = g.search(q, M, cfg.alpha, cfg.beta, k=cfg.k)
     return db, q, M, res
 
@@ -64,9 +64,14 @@ def test_c2_fullsize_sampled():
     _sampled(cfg, db, q, M, res)
 
 
-def test_c4_fullsize_planted():
+@pytest.mark.parametrize("first_stage", [16, 8])
+def test_c4_fullsize_planted(first_stage):
+    """C4 is the overflow stress config: with the int8 first stage every planted
+    copy saturates and is re-aligned at int16 (R14: int16 cannot saturate here)."""
     cfg = CONFIGS["C4"]
-    db, q, M, res = _search(cfg)
+    db, q, M, res = _search(cfg, first_stage=first_stage)
+    if first_stage == 8:
+        assert res.stats["n_rerun16"] >= 90_000 and res.stats["n_rerun32"] == 0
     _, kind = db_lengths(cfg)
     planted = np.nonzero(kind == 2)[0]
     _properties(cfg, db, q, M, res)

@@ -83,6 +83,41 @@ def test_first_stage_32_equals_oracle():
     _check(db, _query(333, 5), B62, 2, 12, first_stage=32)
 
 
+@pytest.mark.parametrize("first_stage", [8, 32])
+@pytest.mark.parametrize("m", [1, 100, 333, 1000])
+def test_first_stage_8_and_32(first_stage, m):
+    rng = np.random.default_rng(400 + m)
+    db = random_db(40 + m, rng.integers(0, 700, size=1200))
+    r = _check(db, _query(m, 16), B62, 2, 12, first_stage=first_stage)
+    assert r.stats["first_stage"] == first_stage
+
+
+def test_int8_stage_falls_back_when_bytes_do_not_fit():
+    db = random_db(41, np.random.default_rng(1).integers(1, 300, size=300))
+    r = _check(db, _query(200, 17), B62, 2, 300, first_stage=8)       # beta > 255
+    assert r.stats["first_stage"] == 16
+
+
+def test_escalation_chain_8_16_32_exact():
+    """Planted copies whose self-scores straddle LIMIT8 = 255-(s_max+B) = 240 and
+    LIMIT16 = 32756 (BLOSUM62): every score exact, and exactly the subjects above
+    each limit are re-aligned at the next width."""
+    M24 = blosum62()
+    limit8, limit16 = 255 - (11 + 4), 32767 - 11
+    targets = [limit8 - 1, limit8, limit8 + 1, 300, 1000, limit16 - 1, limit16, limit16 + 1, 40000]
+    seqs = [_seq_with_self_score(t, M24) for t in targets]
+    rng = np.random.default_rng(9)
+    lens = np.concatenate([[x.size for x in seqs], rng.integers(1, 400, size=500)])
+    db = random_db(42, lens)
+    for i, x in enumerate(seqs):
+        db.residues[db.offsets[i]:db.offsets[i] + x.size] = x
+    for qi, q in enumerate((seqs[4], seqs[-1])):      # query = one of the planted sequences
+        r = _check(db, q, B62, 2, 12, first_stage=8)
+        ref = oracle.db_scores(q, db, B62, 2, 12)
+        assert r.stats["n_rerun16"] == int((ref > limit8).sum())
+        assert r.stats["n_rerun32"] == int((ref > limit16).sum())
+
+
 @pytest.mark.parametrize("tile_rows", ["32", "48", "64"])
 def test_tile_rows_invariance(tile_rows, monkeypatch):
     """Scores do not depend on the register-tile height (T-invariance)."""
