@@ -62,7 +62,7 @@ int tile_rows_env() {
 int threads_env(int def) {
   const char* e = getenv("SW_THREADS");
   const int v = e ? atoi(e) : def;
-  return (v == 256 || v == 384 || v == 512) ? v : def;
+  return (v == 384 || v == 512) ? v : def;
 }
 
 template <int T, int NT>
@@ -72,7 +72,7 @@ void* inter16_kernel(bool smem) {
 
 template <int T>
 void* inter16_kernel_nt(bool smem, int nt) {
-  return nt == 512 ? inter16_kernel<T, 512>(smem) : nt == 256 ? inter16_kernel<T, 256>(smem) : inter16_kernel<T, 384>(smem);
+  return nt == 512 ? inter16_kernel<T, 512>(smem) : inter16_kernel<T, 384>(smem);
 }
 constexpr int kMaxSmemProfile = 200 * 1024;
 
@@ -598,7 +598,8 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   };
   const int T = tile_rows_env();
   const int nt = threads_env(T == 32 ? 512 : 384);
-  void* kern16 = T == 32 ? inter16_kernel_nt<32>(smem, nt) : T == 48 ? inter16_kernel_nt<48>(smem, nt) : inter16_kernel_nt<64>(smem, nt);
+  void* kern16 = T == 32 ? inter16_kernel_nt<32>(smem, nt) : T == 48 ? inter16_kernel_nt<48>(smem, nt)
+               : inter16_kernel_nt<64>(smem, nt);
   CK(cudaFuncSetAttribute(kern16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
   auto launch16 = [&](const uint2* words, const GroupDesc* groups, int n_groups_i, const int* n_groups_dev,
                       const int* pos_map, int n_long_i, int* counter) -> int {

@@ -150,6 +150,73 @@ struct ResCursor {
 // bnd[j] carries (E(i0,j), H(i0-1,j)) in and (E(i0+R,j), H(i0+R-1,j)) out
 // between tiles (the paper's "tiled SW computation").
 // ---------------------------------------------------------------------------
+// Two consecutive columns A = j and B = j+1 interleaved with a one-row skew:
+// step r does A(row r) and B(row r-1).  B(row r') only needs D[r'], F[r'] as
+// left by A(row r') and B's own E chain, so every step carries two independent
+// dependency chains (the fixed-latency "wait" stall of the single-column loop).
+template <int R>
+__device__ __forceinline__ void col16x2(uint32_t (&D)[R], uint32_t (&F)[R],
+                                        uint32_t& eA, uint32_t htopA, const int8_t* __restrict__ ploA,
+                                        const int8_t* __restrict__ phiA, uint32_t& eB, uint32_t htopB,
+                                        const int8_t* __restrict__ ploB, const int8_t* __restrict__ phiB,
+                                        uint32_t na2, uint32_t nb2, uint32_t& hmax, uint32_t& hlA,
+                                        uint32_t& hlB) {
+  uint32_t hpA = htopA, hpB = htopB, hoA = 0u, hoB = 0u;
+  uint2 aA = *reinterpret_cast<const uint2*>(ploA), bA = *reinterpret_cast<const uint2*>(phiA);
+  uint2 aB = *reinterpret_cast<const uint2*>(ploB), bB = *reinterpret_cast<const uint2*>(phiB);
+  uint2 aBn = aB, bBn = bB;
+#pragma unroll
+  for (int r = 0; r <= R; r++) {
+    if (r < R) {                                   // ---- column A, row r
+      const int rr = r & 7;
+      if (rr == 0 && r > 0) {
+        aA = *reinterpret_cast<const uint2*>(ploA + r);
+        bA = *reinterpret_cast<const uint2*>(phiA + r);
+      }
+      const uint32_t h = __vimax3_s16x2(D[r], eA, F[r]);
+      const uint32_t sn = prmt(rr < 4 ? aA.x : aA.y, rr < 4 ? bA.x : bA.y, sel_pair(rr & 3));
+      D[r] = __vadd2(hpA, sn);
+      const uint32_t hb = __vadd2(h, nb2);
+      eA = __viaddmax_s16x2_relu(eA, na2, hb);
+      F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+      if (rr & 1) hmax = __vimax3_s16x2(hmax, hoA, h);
+      else hoA = h;
+      hpA = h;
+    }
+    if (r >= 1) {                                  // ---- column B, row r-1
+      const int q = r - 1, rr = q & 7;
+      if (rr == 0 && q > 0) {
+        aB = aBn;
+        bB = bBn;
+      }
+      if (rr == 0 && q + 8 < R) {                  // B's next chunk, one chunk ahead
+        aBn = *reinterpret_cast<const uint2*>(ploB + q + 8);
+        bBn = *reinterpret_cast<const uint2*>(phiB + q + 8);
+      }
+      const uint32_t h = __vimax3_s16x2(D[q], eB, F[q]);
+      const uint32_t sn = prmt(rr < 4 ? aB.x : aB.y, rr < 4 ? bB.x : bB.y, sel_pair(rr & 3));
+      D[q] = __vadd2(hpB, sn);
+      const uint32_t hb = __vadd2(h, nb2);
+      eB = __viaddmax_s16x2_relu(eB, na2, hb);
+      F[q] = __viaddmax_s16x2_relu(F[q], na2, hb);
+      if (rr & 1) hmax = __vimax3_s16x2(hmax, hoB, h);
+      else hoB = h;
+      hpB = h;
+    }
+  }
+  hlA = hpA;
+  hlB = hpB;
+}
+
+// Packed residue pair (lo, hi codes) of column c of this lane: word c/6, field c%6.
+__device__ __forceinline__ uint2 res_word(const uint2* __restrict__ lw, int c, int nwords) {
+  const int w = (int)(__umulhi((unsigned)c, 0xAAAAAAABu) >> 2);   // c / 6
+  return w < nwords ? __ldg(lw + (long long)w * 32) : make_uint2(kDummyWord, kDummyWord);
+}
+__device__ __forceinline__ int res_shift(int c) {
+  return 5 * (c - 6 * (int)(__umulhi((unsigned)c, 0xAAAAAAABu) >> 2));
+}
+
 template <int R>
 __device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
                                        const int8_t* __restrict__ prof, int stride, int i0,
@@ -159,36 +226,50 @@ __device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
   uint32_t D[R], F[R];
 #pragma unroll
   for (int r = 0; r < R; r++) { D[r] = 0u; F[r] = 0u; }
-  ResCursor rc;
-  rc.init(gw + lane, (ncols + kResPerWord - 1) / kResPerWord);
+  const uint2* lw = gw + lane;
+  const int nwords = (ncols + kResPerWord - 1) / kResPerWord;
+  const int8_t* pr = prof + i0;
   {  // virtual column j = -1 (all-zero boundary): primes D[r] = fsbt(q_{i0+r}, s_0)
+    const uint2 w0 = lw[0];
     uint32_t e0 = 0u;
-    col16<R>(D, F, e0, 0u, prof + rc.lo() * stride + i0, prof + rc.hi() * stride + i0, na2, nb2, hmax);
-    rc.next();
+    col16<R>(D, F, e0, 0u, pr + (w0.x & 31u) * stride, pr + (w0.y & 31u) * stride, na2, nb2, hmax);
   }
-  // Two columns per iteration: the boundary row of column j is loaded two columns
-  // ahead into the register it is consumed from (bE for even, bO for odd j), so
-  // no register copy waits on an in-flight load.
+  // Columns are taken two at a time (A = j, B = j+1).  The residue words of the
+  // next pair's "next columns" (j+3, j+4) and its boundary rows (j+2, j+3) are
+  // loaded one pair ahead into the registers they are consumed from.
   const uint2 z = make_uint2(0u, 0u);
   uint2 bE = first ? z : bnd[lane];
   uint2 bO = (first || ncols < 2) ? z : bnd[32 + lane];
-  for (int j = 0; j < ncols; j += 2) {
-    {
-      uint32_t e = bE.x;                                          // E(i0, j)
-      const uint32_t hl = col16<R>(D, F, e, bE.y, prof + rc.lo() * stride + i0,
-                                   prof + rc.hi() * stride + i0, na2, nb2, hmax);
-      if (!first && j + 2 < ncols) bE = bnd[(j + 2) * 32 + lane];
-      if (!last) bnd[j * 32 + lane] = make_uint2(e, hl);
-      rc.next();
+  uint2 wA = res_word(lw, 1, nwords), wB = res_word(lw, 2, nwords);
+  int j = 0;
+  for (; j + 1 < ncols; j += 2) {
+    const int shA = res_shift(j + 1), shB = res_shift(j + 2);
+    uint32_t eA = bE.x, eB = bO.x, hlA, hlB;
+#ifdef SW_INTERLEAVE_COLUMNS
+    col16x2<R>(D, F, eA, bE.y, pr + ((wA.x >> shA) & 31u) * stride, pr + ((wA.y >> shA) & 31u) * stride,
+               eB, bO.y, pr + ((wB.x >> shB) & 31u) * stride, pr + ((wB.y >> shB) & 31u) * stride,
+               na2, nb2, hmax, hlA, hlB);
+#else
+    hlA = col16<R>(D, F, eA, bE.y, pr + ((wA.x >> shA) & 31u) * stride, pr + ((wA.y >> shA) & 31u) * stride,
+                   na2, nb2, hmax);
+    hlB = col16<R>(D, F, eB, bO.y, pr + ((wB.x >> shB) & 31u) * stride, pr + ((wB.y >> shB) & 31u) * stride,
+                   na2, nb2, hmax);
+#endif
+    wA = res_word(lw, j + 3, nwords);
+    wB = res_word(lw, j + 4, nwords);
+    if (!first && j + 2 < ncols) bE = bnd[(j + 2) * 32 + lane];
+    if (!first && j + 3 < ncols) bO = bnd[(j + 3) * 32 + lane];
+    if (!last) {
+      bnd[j * 32 + lane] = make_uint2(eA, hlA);
+      bnd[(j + 1) * 32 + lane] = make_uint2(eB, hlB);
     }
-    if (j + 1 < ncols) {
-      uint32_t e = bO.x;                                          // E(i0, j+1)
-      const uint32_t hl = col16<R>(D, F, e, bO.y, prof + rc.lo() * stride + i0,
-                                   prof + rc.hi() * stride + i0, na2, nb2, hmax);
-      if (!first && j + 3 < ncols) bO = bnd[(j + 3) * 32 + lane];
-      if (!last) bnd[(j + 1) * 32 + lane] = make_uint2(e, hl);
-      rc.next();
-    }
+  }
+  if (j < ncols) {                                 // odd tail column
+    const int shA = res_shift(j + 1);
+    uint32_t e = bE.x;
+    const uint32_t hl = col16<R>(D, F, e, bE.y, pr + ((wA.x >> shA) & 31u) * stride,
+                                 pr + ((wA.y >> shA) & 31u) * stride, na2, nb2, hmax);
+    if (!last) bnd[j * 32 + lane] = make_uint2(e, hl);
   }
 }
 
