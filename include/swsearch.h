@@ -145,6 +145,24 @@ int sw_search_async(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t*
                     int64_t* d_topk_ids, int32_t* d_topk_scores, void* stream);
 
 /*
+ * Batched search (the paper's protocol searches 20
+ * queries against one database): every query against every
+ * subject, results identical to n_queries calls of sw_search.  Queries are
+ * paired by length; a pair is aligned in ONE pass with the two queries in the
+ * lo/hi halves of int16x2 (the substitution pair is then one word of a pair
+ * profile), each query's saturated subjects are rerun in int32.  Pairs whose
+ * pair profile would not fit shared memory (longer query > ~2000) and an odd
+ * last query run as single searches.  Blocking; host buffers.
+ *   queries    host, concatenated codes 0..23; query q = queries[qoffsets[q] .. +qlens[q])
+ *   scores     host int32[n_queries][n_seqs] (query-major, input order) or NULL
+ *   topk_ids / topk_scores  host [n_queries][k] or NULL
+ *   stats      aggregate (cells over all queries; reserved[0] = pairs aligned jointly)
+ */
+int sw_search_batch(sw_db* db, const uint8_t* queries, const int64_t* qoffsets, const int32_t* qlens,
+                    int32_t n_queries, const int8_t* matrix, int32_t alpha, int32_t beta, int32_t k,
+                    int32_t* scores, int64_t* topk_ids, int32_t* topk_scores, sw_stats* stats);
+
+/*
  * Merge n_lists top-k lists (host; e.g. one per GPU after an all-gather) into
  * the global top-k by (score desc, id asc).  Entries with id < 0 are ignored.
  *   ids/scores   host, n_lists * k_in entries (list-major)

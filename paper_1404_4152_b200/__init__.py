@@ -56,7 +56,7 @@ class sw_db_info(ctypes.Structure):
 
 
 # Every symbol include/swsearch.h declares (tests check the .so exports all of them).
-EXPORTS = ("sw_opts_default", "sw_db_create", "sw_search", "sw_search_async", "sw_merge_topk",
+EXPORTS = ("sw_opts_default", "sw_db_create", "sw_search", "sw_search_async", "sw_search_batch", "sw_merge_topk",
            "sw_db_get_info", "sw_db_stage_times", "sw_db_destroy", "sw_strerror", "sw_last_error")
 
 _lib = None
@@ -78,6 +78,8 @@ def lib() -> ctypes.CDLL:
         L.sw_search.restype = ctypes.c_int
         L.sw_search_async.argtypes = [P, P, i32, P, i32, i32, i32, P, P, P, P]
         L.sw_search_async.restype = ctypes.c_int
+        L.sw_search_batch.argtypes = [P, P, P, P, i32, P, i32, i32, i32, P, P, P, ctypes.POINTER(sw_stats)]
+        L.sw_search_batch.restype = ctypes.c_int
         L.sw_merge_topk.argtypes = [P, P, i32, i32, i32, P, P]
         L.sw_merge_topk.restype = ctypes.c_int
         L.sw_db_get_info.argtypes = [P, ctypes.POINTER(sw_db_info)]
@@ -173,6 +175,26 @@ class Database:
         _check(lib().sw_search(self._h, _ptr(q), q.size, _ptr(M), alpha, beta, k, _ptr(sc), _ptr(ti),
                                _ptr(ts), ctypes.byref(st)))
         return SearchResult(sc, ti, ts, st.as_dict())
+
+    def search_batch(self, queries, matrix, alpha: int, beta: int, k: int = 10, scores: bool = True):
+        """sw_search_batch: a list of query code arrays -> SearchResult with
+        scores (n_queries, n_seqs), topk_ids/topk_scores (n_queries, k)."""
+        qs = [np.ascontiguousarray(q, dtype=np.uint8) for q in queries]
+        cat = np.concatenate(qs) if qs else np.zeros(0, np.uint8)
+        lens = np.array([q.size for q in qs], dtype=np.int32)
+        offs = np.zeros(len(qs), dtype=np.int64)
+        if len(qs) > 1:
+            np.cumsum(lens[:-1], out=offs[1:])
+        M = np.ascontiguousarray(matrix, dtype=np.int8)
+        sc = np.empty((len(qs), self.n_seqs), dtype=np.int32) if scores else None
+        ti = np.empty((len(qs), k), dtype=np.int64)
+        ts = np.empty((len(qs), k), dtype=np.int32)
+        st = sw_stats()
+        _check(lib().sw_search_batch(self._h, _ptr(cat) if cat.size else None, _ptr(offs), _ptr(lens), len(qs),
+                                     _ptr(M), alpha, beta, k, _ptr(sc), _ptr(ti), _ptr(ts), ctypes.byref(st)))
+        d = st.as_dict()
+        d["pairs"] = st.reserved[0]
+        return SearchResult(sc, ti, ts, d)
 
     def search_async(self, query, matrix, alpha: int, beta: int, k: int, d_scores=None, d_topk_ids=None,
                      d_topk_scores=None, stream=None):

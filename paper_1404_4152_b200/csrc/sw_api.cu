@@ -144,6 +144,13 @@ struct sw_db {
   GroupDesc* d_mgroups = nullptr; // mini-group layout of the int8-flagged subjects
   uint2* d_mwords = nullptr;
   uint8_t* d_prof8b = nullptr;    // biased uint8 profile of the int8 stage
+  // f1 batched queries: second query's int8 profile, pair profile, its scores and flags
+  int8_t* d_prof_b = nullptr;
+  size_t prof_b_cap = 0;
+  uint32_t* d_prof2 = nullptr;
+  size_t prof2_cap = 0;
+  int* d_score_sorted2 = nullptr;
+  uint8_t* d_flag_b = nullptr;
   int* d_counters = nullptr;      // work counters: [0] first pass, [2] int32 list, [3] cand count, [4] int16 rerun
   unsigned* d_hist = nullptr;
   swk::SelState* d_sel = nullptr;
@@ -198,6 +205,7 @@ static void free_db(sw_db* db) {
                   db->d_query, db->d_matrix, db->d_prof, db->d_score_sorted, db->d_scores, db->d_keys,
                   db->d_cand, db->d_cand2, db->d_flag8, db->d_flag16, db->d_list8, db->d_list16,
                   db->d_block_counts, db->d_cnt, db->d_mini_sizes, db->d_mgroups, db->d_mwords, db->d_prof8b,
+                  db->d_prof_b, db->d_prof2, db->d_score_sorted2, db->d_flag_b,
                   db->d_counters, db->d_hist, db->d_sel,
                   db->d_topk_ids, db->d_topk_scores, db->d_cub};
   for (void* p : ptrs)
@@ -516,6 +524,67 @@ static int ensure(void** p, size_t* cap, size_t need) {
   return SW_OK;
 }
 
+// Stage (iv) for one query: scatter the sorted-order scores to input order and
+// select the exact top-k by (score desc, global id asc) -- "sort all alignment
+// scores in descending order" without sorting all N.
+static int rank_enqueue(sw_db* db, const int* score_sorted, int* d_scores, int32_t k, long long* d_tk_ids,
+                        int* d_tk_scores, cudaStream_t st, int64_t& nl) {
+  const int n = (int)db->n_seqs;
+  if (n > 0) {
+    const int fb = std::min((n + 255) / 256, db->num_sms * 8);
+    swk::k_finalize<<<fb, 256, 0, st>>>(score_sorted, db->d_perm, n, db->d_gid, d_scores, db->d_keys);
+    CK(cudaGetLastError());
+    nl++;
+  }
+  if (d_tk_ids || d_tk_scores) {
+    const int cnt = std::min<int64_t>(k, n);
+    if (cnt > 0) {
+      const bool take_all = k >= n;
+      if (!take_all) {
+        swk::k_sel_init<<<1, 32, 0, st>>>(db->d_sel, (long long)k);
+        nl++;
+        const int hb = std::min((n + 1023) / 1024, db->num_sms * 4);
+        for (int shift = 56; shift >= 0; shift -= 8) {
+          swk::k_sel_hist<<<hb, 256, 0, st>>>(db->d_keys, n, db->d_sel, shift, db->d_hist);
+          swk::k_sel_pick<<<1, 256, 0, st>>>(db->d_sel, shift, db->d_hist);
+          nl += 2;
+        }
+        CK(cudaGetLastError());
+      }
+      if (db->cand_cap < cnt) {
+        if (db->d_cand) cudaFree(db->d_cand);
+        if (db->d_cand2) cudaFree(db->d_cand2);
+        db->d_cand = db->d_cand2 = nullptr;
+        CK(cudaMalloc(&db->d_cand, (size_t)cnt * sizeof(unsigned long long)));
+        CK(cudaMalloc(&db->d_cand2, (size_t)cnt * sizeof(unsigned long long)));
+        db->cand_cap = cnt;
+      }
+      const int cb = std::min((n + 1023) / 1024, db->num_sms * 4);
+      CK(cudaMemsetAsync(db->d_counters + 3, 0, sizeof(int), st));   // candidate count (per ranking)
+      swk::k_sel_compact<<<cb, 256, 0, st>>>(db->d_keys, n, db->d_sel, take_all ? 1 : 0, db->d_cand,
+                                            db->d_counters + 3);
+      CK(cudaGetLastError());
+      nl += 2;   // compaction + final sort/decode
+      if (cnt <= 4096) {
+        swk::k_topk_small<<<1, 1024, 0, st>>>(db->d_cand, cnt, k, d_tk_ids, d_tk_scores);
+      } else {
+        size_t need = 0;
+        cub::DeviceRadixSort::SortKeysDescending(nullptr, need, db->d_cand, db->d_cand2, cnt, 0, 64, st);
+        int rc = ensure(&db->d_cub, &db->cub_bytes, need);
+        if (rc) return rc;
+        CK(cub::DeviceRadixSort::SortKeysDescending(db->d_cub, need, db->d_cand, db->d_cand2, cnt, 0, 64, st));
+        swk::k_topk_decode<<<(k + 255) / 256, 256, 0, st>>>(db->d_cand2, cnt, k, d_tk_ids, d_tk_scores);
+      }
+      CK(cudaGetLastError());
+    } else {
+      swk::k_topk_decode<<<(k + 255) / 256, 256, 0, st>>>(db->d_cand, 0, k, d_tk_ids, d_tk_scores);
+      CK(cudaGetLastError());
+      nl++;
+    }
+  }
+  return SW_OK;
+}
+
 // Enqueue the whole search on `st`.  Outputs: d_scores (input order) may be
 // nullptr; top-k always goes to d_tk_ids/d_tk_scores when non-null.
 static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix,
@@ -675,56 +744,9 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   CK(cudaEventRecord(ev[3], st));
 
   // ---- stage (iv): scatter + exact top-k ----
-  if (n > 0) {
-    const int fb = std::min((n + 255) / 256, db->num_sms * 8);
-    swk::k_finalize<<<fb, 256, 0, st>>>(db->d_score_sorted, db->d_perm, n, db->d_gid, d_scores, db->d_keys);
-    CK(cudaGetLastError());
-    nl++;
-  }
-  if (d_tk_ids || d_tk_scores) {
-    const int cnt = std::min<int64_t>(k, n);
-    if (cnt > 0) {
-      const bool take_all = k >= n;
-      if (!take_all) {
-        swk::k_sel_init<<<1, 32, 0, st>>>(db->d_sel, (long long)k);
-        nl++;
-        const int hb = std::min((n + 1023) / 1024, db->num_sms * 4);
-        for (int shift = 56; shift >= 0; shift -= 8) {
-          swk::k_sel_hist<<<hb, 256, 0, st>>>(db->d_keys, n, db->d_sel, shift, db->d_hist);
-          swk::k_sel_pick<<<1, 256, 0, st>>>(db->d_sel, shift, db->d_hist);
-          nl += 2;
-        }
-        CK(cudaGetLastError());
-      }
-      if (db->cand_cap < cnt) {
-        if (db->d_cand) cudaFree(db->d_cand);
-        if (db->d_cand2) cudaFree(db->d_cand2);
-        db->d_cand = db->d_cand2 = nullptr;
-        CK(cudaMalloc(&db->d_cand, (size_t)cnt * sizeof(unsigned long long)));
-        CK(cudaMalloc(&db->d_cand2, (size_t)cnt * sizeof(unsigned long long)));
-        db->cand_cap = cnt;
-      }
-      const int cb = std::min((n + 1023) / 1024, db->num_sms * 4);
-      swk::k_sel_compact<<<cb, 256, 0, st>>>(db->d_keys, n, db->d_sel, take_all ? 1 : 0, db->d_cand,
-                                            db->d_counters + 3);
-      CK(cudaGetLastError());
-      nl += 2;   // compaction + final sort/decode
-      if (cnt <= 4096) {
-        swk::k_topk_small<<<1, 1024, 0, st>>>(db->d_cand, cnt, k, d_tk_ids, d_tk_scores);
-      } else {
-        size_t need = 0;
-        cub::DeviceRadixSort::SortKeysDescending(nullptr, need, db->d_cand, db->d_cand2, cnt, 0, 64, st);
-        int rc = ensure(&db->d_cub, &db->cub_bytes, need);
-        if (rc) return rc;
-        CK(cub::DeviceRadixSort::SortKeysDescending(db->d_cub, need, db->d_cand, db->d_cand2, cnt, 0, 64, st));
-        swk::k_topk_decode<<<(k + 255) / 256, 256, 0, st>>>(db->d_cand2, cnt, k, d_tk_ids, d_tk_scores);
-      }
-      CK(cudaGetLastError());
-    } else {
-      swk::k_topk_decode<<<(k + 255) / 256, 256, 0, st>>>(db->d_cand, 0, k, d_tk_ids, d_tk_scores);
-      CK(cudaGetLastError());
-      nl++;
-    }
+  {
+    int rc = rank_enqueue(db, db->d_score_sorted, d_scores, k, d_tk_ids, d_tk_scores, st, nl);
+    if (rc) return rc;
   }
   CK(cudaEventRecord(ev[4], st));
   CK(cudaEventRecord(db->ev_done, st));
@@ -803,6 +825,203 @@ int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matri
     cudaEventElapsedTime(&ms, ev[2], ev[3]); stats->ms_rerun = ms;
     cudaEventElapsedTime(&ms, ev[3], ev[4]); stats->ms_finalize = ms;
     stats->first_stage = db->last_first_stage;
+  }
+  return SW_OK;
+}
+
+
+// ---- f1: batched queries, two per pass ----
+constexpr int kMaxPairStride = kMaxSmemProfile / (4 * swk::kProfRows);   // words per pair-profile row
+
+static int pair_fits(int ma, int mb) {
+  const int m_pad = (std::max(ma, mb) + 7) / 8 * 8;
+  return (m_pad + 31) / 32 * 32 + 1 <= kMaxPairStride;
+}
+
+// Align queries a and b against every subject in ONE inter-task pass (lo/hi
+// halves of int16x2 = the two queries, one subject per lane), then rerun each
+// query's saturated subjects in int32.  Sorted-order scores land in
+// d_score_sorted (a) and d_score_sorted2 (b).
+static int pair_enqueue(sw_db* db, const uint8_t* qa, int ma, const uint8_t* qb, int mb, const int8_t* matrix,
+                        int alpha, int beta, int smax, cudaStream_t st, int64_t& nl) {
+  const int n = (int)db->n_seqs;
+  const int m_pad = (std::max(ma, mb) + 7) / 8 * 8;
+  const int stride2 = (m_pad + 31) / 32 * 32 + 1;                 // odd word stride: conflict-free LDS.32
+  const int mpa = (ma + 7) / 8 * 8, mpb = (mb + 7) / 8 * 8;
+  const int sa = (mpa + 31) / 32 * 32 + 8, sb = (mpb + 31) / 32 * 32 + 8;
+  const size_t pa = ((size_t)swk::kProfRows * sa + 15) / 16 * 16, pb = ((size_t)swk::kProfRows * sb + 15) / 16 * 16;
+  const size_t p2 = (size_t)swk::kProfRows * stride2 * sizeof(uint32_t);
+  {
+    const size_t need = (size_t)ma + mb + 1024;
+    if (db->stage_cap < need) {
+      if (db->h_stage) { cudaEventSynchronize(db->ev_stage); cudaFreeHost(db->h_stage); db->h_stage = nullptr; }
+      CK(cudaHostAlloc(&db->h_stage, need, cudaHostAllocDefault));
+      db->stage_cap = need;
+    } else {
+      CK(cudaEventSynchronize(db->ev_stage));
+    }
+    memcpy(db->h_stage, matrix, 1024);
+    memcpy(db->h_stage + 1024, qa, ma);
+    memcpy(db->h_stage + 1024 + ma, qb, mb);
+    size_t qcap = (size_t)db->query_cap;
+    void* v = db->d_query;
+    int rc = ensure(&v, &qcap, (size_t)ma + mb);
+    db->d_query = (uint8_t*)v;
+    db->query_cap = (int)qcap;
+    if (rc) return rc;
+    v = db->d_prof;
+    rc = ensure(&v, &db->prof_cap, pa);
+    db->d_prof = (int8_t*)v;
+    if (rc) return rc;
+    v = db->d_prof_b;
+    rc = ensure(&v, &db->prof_b_cap, pb);
+    db->d_prof_b = (int8_t*)v;
+    if (rc) return rc;
+    v = db->d_prof2;
+    rc = ensure(&v, &db->prof2_cap, p2);
+    db->d_prof2 = (uint32_t*)v;
+    if (rc) return rc;
+    if (!db->d_score_sorted2) CK(cudaMalloc(&db->d_score_sorted2, std::max<int64_t>(n, 1) * sizeof(int)));
+    if (!db->d_flag_b) CK(cudaMalloc(&db->d_flag_b, std::max<int64_t>(n, 1)));
+    CK(cudaMemcpyAsync(db->d_matrix, db->h_stage, 1024, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(db->d_query, db->h_stage + 1024, (size_t)ma + mb, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(db->ev_stage, st));
+  }
+  const uint8_t* dqa = db->d_query;
+  const uint8_t* dqb = db->d_query + ma;
+  swk::k_profile<<<64, 256, 0, st>>>(dqa, ma, db->d_matrix, db->d_prof, sa);
+  swk::k_profile<<<64, 256, 0, st>>>(dqb, mb, db->d_matrix, db->d_prof_b, sb);
+  swk::k_profile_pair<<<64, 256, 0, st>>>(dqa, ma, dqb, mb, db->d_matrix, db->d_prof2, stride2);
+  CK(cudaMemsetAsync(db->d_counters, 0, 8 * sizeof(int), st));
+  CK(cudaMemsetAsync(db->d_cnt, 0, 4 * sizeof(int), st));
+  CK(cudaMemsetAsync(db->d_flag16, 0, (size_t)std::max(n, 1), st));
+  CK(cudaMemsetAsync(db->d_flag_b, 0, (size_t)std::max(n, 1), st));
+  nl += 3;
+  const int grid = db->num_sms;
+  const int limit16 = 32767 - smax;
+  if (n > 0) {
+    CK(cudaFuncSetAttribute(swk::k_multi16<kTileRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2));
+    swk::k_multi16<kTileRows><<<grid, swk::kInterThreads, p2, st>>>(
+        db->d_words, db->d_groups, (int)db->n_groups, db->d_prof2, m_pad, stride2, alpha, beta, limit16,
+        db->d_scratch, db->scratch_cols, db->d_counters + 0, db->d_score_sorted, db->d_score_sorted2,
+        db->d_flag16, db->d_flag_b);
+    CK(cudaGetLastError());
+    nl++;
+    const int nb_scan = std::max(1, (n + swk::kScanBlock - 1) / swk::kScanBlock);
+    for (int which = 0; which < 2; which++) {
+      uint8_t* flag = which ? db->d_flag_b : db->d_flag16;
+      int* cnt = db->d_cnt + (which ? 3 : 1);
+      swk::k_flag_count<<<nb_scan, swk::kScanBlock, 0, st>>>(flag, n, db->d_block_counts);
+      swk::k_scan_exclusive<<<1, swk::kScanBlock, 0, st>>>(db->d_block_counts, nb_scan, cnt, nullptr);
+      swk::k_flag_scatter<<<nb_scan, swk::kScanBlock, 0, st>>>(flag, n, db->d_block_counts, db->d_list16);
+      const int mp = which ? mpb : mpa, sw_ = which ? sb : sa;
+      const size_t pbytes = which ? pb : pa;
+      const bool smem = pbytes <= (size_t)kMaxSmemProfile;
+      auto k32 = smem ? swk::k_list32<kTileRows, true> : swk::k_list32<kTileRows, false>;
+      CK(cudaFuncSetAttribute(k32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem ? pbytes : 0, 1)));
+      k32<<<grid, swk::kInterThreads, smem ? pbytes : 0, st>>>(
+          db->d_words, db->d_groups, db->d_list16, cnt, 0, db->d_len_sorted, which ? db->d_prof_b : db->d_prof, mp,
+          sw_, alpha, beta, db->d_scratch, db->scratch_cols, db->d_counters + (which ? 5 : 2),
+          which ? db->d_score_sorted2 : db->d_score_sorted);
+      CK(cudaGetLastError());
+      nl += 4;
+    }
+  }
+  return SW_OK;
+}
+
+int sw_search_batch(sw_db* db, const uint8_t* queries, const int64_t* qoffsets, const int32_t* qlens,
+                    int32_t n_queries, const int8_t* matrix, int32_t alpha, int32_t beta, int32_t k,
+                    int32_t* scores, int64_t* topk_ids, int32_t* topk_scores, sw_stats* stats) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (!db) return fail(SW_EINVAL, "db is NULL");
+  if (n_queries < 1 || !queries || !qoffsets || !qlens) return fail(SW_EINVAL, "need n_queries >= 1 and non-NULL query arrays");
+  int smax = 0, smin = 0;
+  for (int q = 0; q < n_queries; q++) {
+    if (qoffsets[q] < 0) return fail(SW_EINVAL, "query %d: negative offset", q);
+    int rc = validate_search(db, queries + qoffsets[q], qlens[q], matrix, alpha, beta, k, &smax, &smin);
+    if (rc) {
+      std::string m = g_last_error;
+      return fail(rc, "query %d: %s", q, m.c_str());
+    }
+  }
+  std::lock_guard<std::mutex> lock(db->mu);
+  CK(cudaSetDevice(db->device));
+  cudaStream_t st = db->stream;
+  if (db->topk_cap < k) {
+    if (db->d_topk_ids) cudaFree(db->d_topk_ids);
+    if (db->d_topk_scores) cudaFree(db->d_topk_scores);
+    db->d_topk_ids = nullptr;
+    db->d_topk_scores = nullptr;
+    CK(cudaMalloc(&db->d_topk_ids, (size_t)k * sizeof(long long)));
+    CK(cudaMalloc(&db->d_topk_scores, (size_t)k * sizeof(int)));
+    db->topk_cap = k;
+  }
+  const int64_t n = db->n_seqs;
+  // queries whose pair profile fits shared memory are paired by length; the rest run singly
+  std::vector<int> order;
+  for (int q = 0; q < n_queries; q++)
+    if (pair_fits(qlens[q], qlens[q])) order.push_back(q);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return qlens[x] > qlens[y]; });
+  if (order.size() % 2) order.push_back(-1);   // odd one out runs singly
+  for (int q = 0; q < n_queries; q++)
+    if (!pair_fits(qlens[q], qlens[q])) { order.push_back(q); order.push_back(-1); }
+  const int n_slots = (int)order.size();
+  std::vector<int> cnt_host(4 * (size_t)n_slots, 0);
+  int64_t nl = 0, n_rerun32 = 0, n_pairs = 0;
+  auto fetch = [&](int q, const int* score_sorted) -> int {
+    int rc = rank_enqueue(db, score_sorted, db->d_scores, k, db->d_topk_ids, db->d_topk_scores, st, nl);
+    if (rc) return rc;
+    if (scores && n) CK(cudaMemcpyAsync(scores + (size_t)q * n, db->d_scores, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (topk_ids) CK(cudaMemcpyAsync(topk_ids + (size_t)q * k, db->d_topk_ids, (size_t)k * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    if (topk_scores) CK(cudaMemcpyAsync(topk_scores + (size_t)q * k, db->d_topk_scores, (size_t)k * sizeof(int), cudaMemcpyDeviceToHost, st));
+    return SW_OK;
+  };
+  for (int t = 0; t < n_slots; t += 2) {
+    const int a = order[t];
+    const int b = order[t + 1];
+    if (a >= 0 && b >= 0) {
+      int rc = pair_enqueue(db, queries + qoffsets[a], qlens[a], queries + qoffsets[b], qlens[b], matrix, alpha, beta,
+                            smax, st, nl);
+      if (rc) return rc;
+      CK(cudaMemcpyAsync(&cnt_host[4 * (size_t)t], db->d_cnt, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      if ((rc = fetch(a, db->d_score_sorted))) return rc;
+      if ((rc = fetch(b, db->d_score_sorted2))) return rc;
+      n_pairs++;
+    } else {
+      for (int q : {a, b}) {
+        if (q < 0) continue;
+        int rc = search_enqueue(db, queries + qoffsets[q], qlens[q], matrix, alpha, beta, k, smax, smin, db->d_scores,
+                                db->d_topk_ids, db->d_topk_scores, st);
+        if (rc) return rc;
+        if (scores && n) CK(cudaMemcpyAsync(scores + (size_t)q * n, db->d_scores, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (topk_ids) CK(cudaMemcpyAsync(topk_ids + (size_t)q * k, db->d_topk_ids, (size_t)k * sizeof(long long), cudaMemcpyDeviceToHost, st));
+        if (topk_scores) CK(cudaMemcpyAsync(topk_scores + (size_t)q * k, db->d_topk_scores, (size_t)k * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        int c[4];
+        CK(cudaMemcpy(c, db->d_cnt, sizeof c, cudaMemcpyDeviceToHost));
+        n_rerun32 += c[1];
+      }
+    }
+    CK(cudaStreamSynchronize(st));   // cnt_host (pageable) and the staging buffer are reused per pair
+  }
+  CK(cudaEventRecord(db->ev_done, st));
+  CK(cudaStreamSynchronize(st));
+  for (int t = 0; t < n_slots; t += 2) n_rerun32 += cnt_host[4 * (size_t)t + 1] + cnt_host[4 * (size_t)t + 3];
+  db->launches += nl;
+  const auto t1 = std::chrono::steady_clock::now();
+  if (stats) {
+    memset(stats, 0, sizeof *stats);
+    int64_t qsum = 0;
+    for (int q = 0; q < n_queries; q++) qsum += qlens[q];
+    stats->cells = qsum * db->sum_len;
+    stats->n_seqs = n;
+    stats->n_inter = n;
+    stats->n_rerun32 = n_rerun32;
+    stats->seconds = std::chrono::duration<double>(t1 - t0).count();
+    stats->gcups = stats->seconds > 0 ? (double)stats->cells / stats->seconds / 1e9 : 0.0;
+    stats->first_stage = 16;
+    stats->reserved[0] = (int32_t)n_pairs;   // query pairs aligned in one pass
   }
   return SW_OK;
 }

@@ -250,3 +250,40 @@ def test_search_validation_errors():
         with pytest.raises(sw.SwError) as ei:
             g.search(qbig, Mbig, 2, 12, k=2)
         assert ei.value.code == sw.SW_ERANGE
+
+
+def test_batched_queries_equal_single_searches():
+    """f1: queries paired in one int16x2 pass give exactly the per-query oracle
+    scores and top-k (odd count, unequal lengths, one query too long to pair)."""
+    rng = np.random.default_rng(77)
+    db = random_db(77, np.concatenate([rng.integers(0, 900, size=1500), [0, 1, 5000]]))
+    qs = [_query(m, 30 + i) for i, m in enumerate([1, 100, 333, 464, 47, 2600, 129])]
+    with sw.Database.from_synth(db, device=0) as g:
+        r = g.search_batch(qs, B62, 2, 12, k=12)
+    assert r.stats["pairs"] == 3
+    for i, q in enumerate(qs):
+        ref = oracle.db_scores(q, db, B62, 2, 12)
+        assert np.array_equal(r.scores[i], ref), i
+        ti, ts = oracle.topk(ref, 12)
+        assert np.array_equal(r.topk_ids[i], ti) and np.array_equal(r.topk_scores[i], ts)
+
+
+def test_batched_queries_saturation_reruns():
+    """Both halves of a query pair saturate independently and are rerun exactly
+    (matrix with diagonal 30 so that ~1,100-residue self-alignments pass LIMIT16)."""
+    M = B62.copy()
+    for c in range(20):
+        M[c, c] = 30
+    qa, qb = _query(1200, 50), _query(1050, 51)       # self-scores 36,000 and 31,500 (row dominance)
+    lens = np.array([qa.size, qb.size, 100, 200, 0])
+    db = random_db(78, lens)
+    db.residues[db.offsets[0]:db.offsets[0] + qa.size] = qa
+    db.residues[db.offsets[1]:db.offsets[1] + qb.size] = qb
+    with sw.Database.from_synth(db, device=0) as g:
+        r = g.search_batch([qa, qb], M, 2, 12, k=2)
+    assert r.stats["pairs"] == 1
+    refs = [oracle.db_scores(q, db, M, 2, 12) for q in (qa, qb)]
+    assert refs[0][0] == 36000 and refs[1][1] == 31500
+    for i in range(2):
+        assert np.array_equal(r.scores[i], refs[i])
+    assert r.stats["n_rerun32"] == sum(int((x > 32767 - 30).sum()) for x in refs)

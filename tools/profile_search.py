@@ -36,3 +36,11 @@ for i in range(a.searches):
           f"inter {st['ms_inter']:.3f} rerun {st['ms_rerun']:.3f} final {st['ms_finalize']:.3f} ms  "
           f"kernel GCUPS {st['cells']/st['ms_inter']/1e6:.1f}  reruns {st['n_rerun32']}", flush=True)
 g.close()
+if os.environ.get("SW_BATCH"):
+    qs = [make_query(base, a.m, seed=s) for s in range(int(os.environ["SW_BATCH"]))]
+    g = sw.Database.from_synth(db, device=0, first_stage=a.first_stage)
+    for i in range(a.searches):
+        r = g.search_batch(qs, M, base.alpha, base.beta, k=base.k, scores=False)
+        st = r.stats
+        print(f"batch {len(qs)} queries: {st['seconds']*1e3:.2f} ms wall  {st['gcups']:.1f} GCUPS  pairs {st['pairs']}", flush=True)
+    g.close()
