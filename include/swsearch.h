@@ -121,6 +121,18 @@ int sw_db_create(const uint8_t* residues, int64_t n_residues, const int64_t* off
                  const sw_opts* opts, sw_db** out);
 
 /*
+ * Persistent packed index (the paper builds "index files"
+ * offline that "can be mapped into virtual memory").
+ * sw_db_save writes the packed, length-sorted layout (group table, permutation,
+ * sorted lengths, global ids, 5-bit words) to `path`; sw_db_load mmaps such a
+ * file and uploads it without re-sorting or re-packing.  A truncated, corrupt
+ * or foreign file is rejected with SW_EINVAL before any device work.  Searches
+ * on a loaded handle are identical to searches on the handle that was saved.
+ */
+int sw_db_save(sw_db* db, const char* path);
+int sw_db_load(const char* path, const sw_opts* opts, sw_db** out);
+
+/*
  * Search one query against every subject; blocks until results are on the host.
  *   query        host, qlen codes 0..23
  *   matrix       host, 32*32 int8 (row = query residue)

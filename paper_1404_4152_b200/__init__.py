@@ -57,7 +57,8 @@ class sw_db_info(ctypes.Structure):
 
 # Every symbol include/swsearch.h declares (tests check the .so exports all of them).
 EXPORTS = ("sw_opts_default", "sw_db_create", "sw_search", "sw_search_async", "sw_search_batch", "sw_merge_topk",
-           "sw_db_get_info", "sw_db_stage_times", "sw_db_destroy", "sw_strerror", "sw_last_error")
+           "sw_db_get_info", "sw_db_stage_times", "sw_db_save", "sw_db_load", "sw_db_destroy", "sw_strerror",
+           "sw_last_error")
 
 _lib = None
 
@@ -86,6 +87,10 @@ def lib() -> ctypes.CDLL:
         L.sw_db_get_info.restype = ctypes.c_int
         L.sw_db_stage_times.argtypes = [P, i32, ctypes.POINTER(ctypes.c_float)]
         L.sw_db_stage_times.restype = ctypes.c_int
+        L.sw_db_save.argtypes = [P, ctypes.c_char_p]
+        L.sw_db_save.restype = ctypes.c_int
+        L.sw_db_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(sw_opts), ctypes.POINTER(P)]
+        L.sw_db_load.restype = ctypes.c_int
         L.sw_db_destroy.argtypes = [P]
         L.sw_db_destroy.restype = None
         L.sw_strerror.argtypes = [ctypes.c_int]
@@ -143,6 +148,24 @@ class Database:
     @classmethod
     def from_synth(cls, db, **kw) -> "Database":
         return cls(db.residues, db.offsets, db.lengths, **kw)
+
+    @classmethod
+    def load(cls, path: str, device: int = -1, first_stage: int = 16, long_threshold: int = 0) -> "Database":
+        """sw_db_load: map a file written by save() and upload it (no re-sort / re-pack)."""
+        L = lib()
+        o = sw_opts()
+        L.sw_opts_default(ctypes.byref(o))
+        o.device, o.first_stage, o.long_threshold = device, first_stage, long_threshold
+        h = ctypes.c_void_p()
+        _check(L.sw_db_load(os.fsencode(path), ctypes.byref(o), ctypes.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        self.n_seqs = self.info()["n_seqs"]
+        return self
+
+    def save(self, path: str):
+        """sw_db_save: write the packed, length-sorted layout to `path`."""
+        _check(lib().sw_db_save(self._h, os.fsencode(path)))
 
     def info(self) -> dict:
         i = sw_db_info()

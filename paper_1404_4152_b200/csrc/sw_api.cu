@@ -23,6 +23,10 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include "../../include/swsearch.h"
 #include "sw_kernels.cuh"
@@ -281,6 +285,8 @@ static int validate_db(const uint8_t* residues, int64_t n_residues, const int64_
   return SW_OK;
 }
 
+static int finish_create(sw_db* db);
+
 static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_t* offsets,
                        const int32_t* lengths, int64_t n_seqs, const int64_t* gids, const sw_opts* o,
                        sw_db* db) {
@@ -411,6 +417,12 @@ static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_
     CK(cudaMemcpy(db->d_gid, gids, n_seqs * sizeof(long long), cudaMemcpyHostToDevice));
   }
 
+  return finish_create(db);
+}
+
+// Device buffers that depend only on the layout (shared by create and load).
+static int finish_create(sw_db* db) {
+  const int64_t n_seqs = db->n_seqs;
   // ---- DP boundary scratch: one slab per resident warp of the persistent kernels ----
   db->scratch_slots = db->num_sms * (swk::kMaxThreads / 32);
   db->scratch_cols = ((int64_t)db->max_inter_len + swk::kResPerWord) / swk::kResPerWord * swk::kResPerWord + swk::kResPerWord;
@@ -479,6 +491,188 @@ int sw_db_create(const uint8_t* residues, int64_t n_residues, const int64_t* off
     return rc;
   }
   int rc = create_impl(residues, n_residues, offsets, lengths, n_seqs, global_ids, &o, db);
+  if (rc != SW_OK) {
+    std::string msg = g_last_error;
+    free_db(db);
+    g_last_error = msg;
+    return rc;
+  }
+  *out = db;
+  return SW_OK;
+}
+
+
+// ---- f2: persistent packed index (the paper's offline, mmap-able index files) ----
+namespace {
+struct DbFileHeader {
+  char magic[8];            // "SWB200DB"
+  uint32_t version;         // 1
+  uint32_t header_bytes;
+  int64_t n_seqs, n_residues, sum_len;
+  int64_t n_groups, n_words;
+  int32_t max_len, has_gid;
+  int64_t off_groups, off_perm, off_len, off_gid, off_words, file_bytes;
+};
+constexpr uint32_t kDbFileVersion = 1;
+int64_t align64(int64_t x) { return (x + 63) / 64 * 64; }
+}  // namespace
+
+int sw_db_save(sw_db* db, const char* path) {
+  if (!db || !path) return fail(SW_EINVAL, "sw_db_save: null argument");
+  std::lock_guard<std::mutex> lock(db->mu);
+  CK(cudaSetDevice(db->device));
+  CK(cudaStreamSynchronize(db->stream));
+  DbFileHeader h;
+  memset(&h, 0, sizeof h);
+  memcpy(h.magic, "SWB200DB", 8);
+  h.version = kDbFileVersion;
+  h.header_bytes = sizeof h;
+  h.n_seqs = db->n_seqs;
+  h.n_residues = db->n_residues;
+  h.sum_len = db->sum_len;
+  h.n_groups = db->n_groups;
+  h.n_words = db->n_words;
+  h.max_len = db->max_len;
+  h.has_gid = db->d_gid ? 1 : 0;
+  h.off_groups = align64(sizeof h);
+  h.off_perm = align64(h.off_groups + h.n_groups * (int64_t)sizeof(GroupDesc));
+  h.off_len = align64(h.off_perm + h.n_seqs * 4);
+  h.off_gid = align64(h.off_len + h.n_seqs * 4);
+  h.off_words = align64(h.off_gid + (h.has_gid ? h.n_seqs * 8 : 0));
+  h.file_bytes = h.off_words + h.n_words * (int64_t)sizeof(uint2);
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(SW_EINVAL, "sw_db_save: cannot open %s for writing", path);
+  int rc = SW_OK;
+  auto put = [&](int64_t off, const void* dev, int64_t bytes) {
+    if (rc != SW_OK || bytes <= 0) return;
+    std::vector<char> buf((size_t)std::min<int64_t>(bytes, 1 << 26));
+    for (int64_t done = 0; done < bytes && rc == SW_OK; done += (int64_t)buf.size()) {
+      const int64_t c = std::min<int64_t>((int64_t)buf.size(), bytes - done);
+      cudaError_t e = cudaMemcpy(buf.data(), (const char*)dev + done, c, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) { rc = fail(SW_ECUDA, "sw_db_save: %s", cudaGetErrorString(e)); return; }
+      if (fseeko(f, off + done, SEEK_SET) != 0 || fwrite(buf.data(), 1, c, f) != (size_t)c)
+        rc = fail(SW_EINVAL, "sw_db_save: write failed on %s", path);
+    }
+  };
+  if (fwrite(&h, sizeof h, 1, f) != 1) rc = fail(SW_EINVAL, "sw_db_save: write failed on %s", path);
+  put(h.off_groups, db->d_groups, h.n_groups * (int64_t)sizeof(GroupDesc));
+  put(h.off_perm, db->d_perm, h.n_seqs * 4);
+  put(h.off_len, db->d_len_sorted, h.n_seqs * 4);
+  if (h.has_gid) put(h.off_gid, db->d_gid, h.n_seqs * 8);
+  put(h.off_words, db->d_words, h.n_words * (int64_t)sizeof(uint2));
+  if (fclose(f) != 0 && rc == SW_OK) rc = fail(SW_EINVAL, "sw_db_save: close failed on %s", path);
+  return rc;
+}
+
+static int load_impl(const char* map, const DbFileHeader& h, sw_db* db) {
+  db->n_seqs = h.n_seqs;
+  db->n_residues = h.n_residues;
+  db->sum_len = h.sum_len;
+  db->max_len = h.max_len;
+  db->n_groups = h.n_groups;
+  db->n_words = h.n_words;
+  db->n_inter = h.n_seqs;
+  db->n_intra = 0;
+  const GroupDesc* groups = (const GroupDesc*)(map + h.off_groups);
+  const int* len_sorted = (const int*)(map + h.off_len);
+  db->max_inter_len = h.n_seqs ? len_sorted[h.n_seqs - 1] : 0;
+  db->group_ncols.resize(h.n_groups);
+  int64_t expect_base = 0;
+  for (int64_t g = 0; g < h.n_groups; g++) {   // the table must describe exactly the stored words
+    db->group_ncols[g] = groups[g].ncols;
+    if (groups[g].base != expect_base || groups[g].ncols < 0 || (g && groups[g].ncols < groups[g - 1].ncols))
+      return fail(SW_EINVAL, "sw_db_load: corrupt group table at group %lld", (long long)g);
+    expect_base += (int64_t)(groups[g].ncols + swk::kResPerWord - 1) / swk::kResPerWord * 32;
+  }
+  if (expect_base != h.n_words) return fail(SW_EINVAL, "sw_db_load: group table / word count mismatch");
+  CK(cudaMalloc(&db->d_words, std::max<int64_t>(h.n_words, 1) * sizeof(uint2)));
+  CK(cudaMalloc(&db->d_groups, std::max<int64_t>(h.n_groups, 1) * sizeof(GroupDesc)));
+  CK(cudaMalloc(&db->d_perm, std::max<int64_t>(h.n_seqs, 1) * sizeof(int)));
+  CK(cudaMalloc(&db->d_len_sorted, std::max<int64_t>(h.n_seqs, 1) * sizeof(int)));
+  // pinned double-buffered staging from the mapped file
+  const int64_t kChunk = 1 << 27;
+  char* stage[2] = {nullptr, nullptr};
+  CK(cudaHostAlloc(&stage[0], kChunk, cudaHostAllocDefault));
+  CK(cudaHostAlloc(&stage[1], kChunk, cudaHostAllocDefault));
+  cudaEvent_t ev[2];
+  cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+  bool used[2] = {false, false};
+  int buf = 0;
+  int rc = SW_OK;
+  auto up = [&](void* dst, const char* src, int64_t bytes) {
+    for (int64_t done = 0; done < bytes && rc == SW_OK; done += kChunk) {
+      const int64_t c = std::min(kChunk, bytes - done);
+      if (used[buf]) cudaEventSynchronize(ev[buf]);
+      memcpy(stage[buf], src + done, c);
+      cudaError_t e = cudaMemcpyAsync((char*)dst + done, stage[buf], c, cudaMemcpyHostToDevice, db->stream);
+      if (e != cudaSuccess) rc = fail(SW_ECUDA, "sw_db_load: %s", cudaGetErrorString(e));
+      cudaEventRecord(ev[buf], db->stream);
+      used[buf] = true;
+      buf ^= 1;
+    }
+  };
+  up(db->d_groups, map + h.off_groups, h.n_groups * (int64_t)sizeof(GroupDesc));
+  up(db->d_perm, map + h.off_perm, h.n_seqs * 4);
+  up(db->d_len_sorted, map + h.off_len, h.n_seqs * 4);
+  if (h.has_gid) {
+    if (cudaMalloc(&db->d_gid, h.n_seqs * sizeof(long long)) != cudaSuccess) rc = fail(SW_ENOMEM, "sw_db_load: gid");
+    up(db->d_gid, map + h.off_gid, h.n_seqs * 8);
+  }
+  up(db->d_words, map + h.off_words, h.n_words * (int64_t)sizeof(uint2));
+  cudaStreamSynchronize(db->stream);
+  cudaFreeHost(stage[0]);
+  cudaFreeHost(stage[1]);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  if (rc != SW_OK) return rc;
+  return finish_create(db);
+}
+
+int sw_db_load(const char* path, const sw_opts* opts, sw_db** out) {
+  if (!out || !path) return fail(SW_EINVAL, "sw_db_load: null argument");
+  *out = nullptr;
+  sw_opts o;
+  sw_opts_default(&o);
+  if (opts) o = *opts;
+  if (o.first_stage != 8 && o.first_stage != 16 && o.first_stage != 32)
+    return fail(SW_EINVAL, "first_stage must be 8, 16 or 32 (got %d)", o.first_stage);
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail(SW_EINVAL, "sw_db_load: cannot open %s", path);
+  struct stat sb;
+  if (fstat(fd, &sb) != 0 || sb.st_size < (off_t)sizeof(DbFileHeader)) {
+    close(fd);
+    return fail(SW_EINVAL, "sw_db_load: %s is not a database file (too small)", path);
+  }
+  void* map = mmap(nullptr, (size_t)sb.st_size, PROT_READ, MAP_PRIVATE, fd, 0);
+  close(fd);
+  if (map == MAP_FAILED) return fail(SW_EINVAL, "sw_db_load: mmap of %s failed", path);
+  DbFileHeader h;
+  memcpy(&h, map, sizeof h);
+  auto bad = [&](const char* why) {
+    munmap(map, (size_t)sb.st_size);
+    return fail(SW_EINVAL, "sw_db_load: %s: %s", path, why);
+  };
+  if (memcmp(h.magic, "SWB200DB", 8) != 0) return bad("bad magic");
+  if (h.version != kDbFileVersion || h.header_bytes != sizeof h) return bad("unsupported version");
+  if (h.n_seqs < 0 || h.n_seqs > 0x7fffffffLL - 64 || h.n_groups != (h.n_seqs + swk::kGroup - 1) / swk::kGroup ||
+      h.n_words < 0 || h.file_bytes != (int64_t)sb.st_size ||
+      h.off_words + h.n_words * (int64_t)sizeof(uint2) != h.file_bytes || h.off_groups < (int64_t)sizeof h ||
+      h.off_perm < h.off_groups + h.n_groups * (int64_t)sizeof(GroupDesc) || h.off_len < h.off_perm + h.n_seqs * 4 ||
+      h.off_gid < h.off_len + h.n_seqs * 4 || h.off_words < h.off_gid + (h.has_gid ? h.n_seqs * 8 : 0))
+    return bad("inconsistent header (truncated or corrupt file)");
+  sw_db* db = new (std::nothrow) sw_db;
+  if (!db) return bad("host allocation");
+  db->first_stage = o.first_stage;
+  db->long_threshold = o.long_threshold;
+  cudaError_t e = cudaSuccess;
+  if (o.device < 0) e = cudaGetDevice(&db->device);
+  else db->device = o.device;
+  if (e == cudaSuccess) e = cudaSetDevice(db->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&db->num_sms, cudaDevAttrMultiProcessorCount, db->device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&db->stream, cudaStreamNonBlocking);
+  int rc = e == cudaSuccess ? load_impl((const char*)map, h, db) : fail(SW_ECUDA, "device %d: %s", db->device, cudaGetErrorString(e));
+  munmap(map, (size_t)sb.st_size);
   if (rc != SW_OK) {
     std::string msg = g_last_error;
     free_db(db);

@@ -82,3 +82,13 @@ def test_merge_topk_matches_oracle_ranking():
     assert np.array_equal(mi, ri) and np.array_equal(ms, rs)
     mi, ms = sw.merge_topk(np.array([[3, -1]]), np.array([[7, -1]]), 3)
     assert mi.tolist() == [3, -1, -1] and ms.tolist() == [7, -1, -1]
+
+
+@pytest.mark.parametrize("content", [None, b"", b"not a database" * 20, b"SWB200DB" + b"\x01\x00\x00\x00" + b"\x00" * 200])
+def test_db_load_rejects_bad_files(tmp_path, content):
+    path = tmp_path / "db.swb"
+    if content is not None:
+        path.write_bytes(content)
+    with pytest.raises(sw.SwError) as ei:
+        sw.Database.load(str(path))
+    assert ei.value.code == sw.SW_EINVAL

@@ -287,3 +287,25 @@ def test_batched_queries_saturation_reruns():
     for i in range(2):
         assert np.array_equal(r.scores[i], refs[i])
     assert r.stats["n_rerun32"] == sum(int((x > 32767 - 30).sum()) for x in refs)
+
+
+def test_persistent_index_roundtrip(tmp_path):
+    """f2: save the packed index, load it (mmap, no re-pack): identical results."""
+    rng = np.random.default_rng(90)
+    db = random_db(90, rng.integers(0, 800, size=3000))
+    gids = rng.permutation(100_000)[:3000].astype(np.int64)
+    q = _query(250, 90)
+    path = str(tmp_path / "db.swb")
+    with sw.Database.from_synth(db, global_ids=gids, device=0) as g:
+        r0 = g.search(q, B62, 2, 12, k=25)
+        g.save(path)
+        info0 = g.info()
+    for fs in (16, 8):
+        with sw.Database.load(path, device=0, first_stage=fs) as h:
+            info1 = h.info()
+            r1 = h.search(q, B62, 2, 12, k=25)
+        assert info1["n_seqs"] == info0["n_seqs"] and info1["packed_bytes"] == info0["packed_bytes"]
+        assert np.array_equal(r0.scores, r1.scores)
+        assert np.array_equal(r0.topk_ids, r1.topk_ids) and np.array_equal(r0.topk_scores, r1.topk_scores)
+    ref = oracle.db_scores(q, db, B62, 2, 12)
+    assert np.array_equal(r1.scores, ref)
