@@ -106,6 +106,8 @@ struct sw_db {
   int device = 0;
   int num_sms = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;     // intra-task kernel beside the inter-task one
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::mutex mu;
   int first_stage = 16;
   int long_threshold = -1;
@@ -121,7 +123,9 @@ struct sw_db {
   int* d_len_sorted = nullptr;    // sorted position -> length
   long long* d_gid = nullptr;     // input index -> global id (nullptr: identity)
 
-  uint2* d_scratch = nullptr;     // DP boundary rows, one slab per resident warp
+  uint2* d_scratch = nullptr;     // DP boundary rows, one slab per resident warp (inter-task kernels)
+  uint2* d_scratch_intra = nullptr; // pass boundaries of the intra-task kernel (runs concurrently: own slabs)
+  long long scratch_cols_intra = 0;
   long long scratch_cols = 0;
   int scratch_slots = 0;
 
@@ -209,7 +213,7 @@ static void free_db(sw_db* db) {
                   db->d_query, db->d_matrix, db->d_prof, db->d_score_sorted, db->d_scores, db->d_keys,
                   db->d_cand, db->d_cand2, db->d_flag8, db->d_flag16, db->d_list8, db->d_list16,
                   db->d_block_counts, db->d_cnt, db->d_mini_sizes, db->d_mgroups, db->d_mwords, db->d_prof8b,
-                  db->d_prof_b, db->d_prof2, db->d_score_sorted2, db->d_flag_b,
+                  db->d_prof_b, db->d_prof2, db->d_score_sorted2, db->d_flag_b, db->d_scratch_intra,
                   db->d_counters, db->d_hist, db->d_sel,
                   db->d_topk_ids, db->d_topk_scores, db->d_cub};
   for (void* p : ptrs)
@@ -220,6 +224,9 @@ static void free_db(sw_db* db) {
   for (auto& set : db->ev_ring)
     for (auto& e : set)
       if (e) cudaEventDestroy(e);
+  if (db->ev_fork) cudaEventDestroy(db->ev_fork);
+  if (db->ev_join) cudaEventDestroy(db->ev_join);
+  if (db->aux) cudaStreamDestroy(db->aux);
   if (db->stream) cudaStreamDestroy(db->stream);
   delete db;
 }
@@ -235,7 +242,8 @@ int sw_db_get_info(const sw_db* db, sw_db_info* info) {
   info->n_intra = db->n_intra;
   info->n_groups = db->n_groups;
   info->packed_bytes = db->n_words * (int64_t)sizeof(uint2);
-  info->scratch_bytes = (int64_t)db->scratch_slots * db->scratch_cols * 32 * (int64_t)sizeof(uint2);
+  info->scratch_bytes = ((int64_t)db->scratch_slots * db->scratch_cols +
+                         (int64_t)db->num_sms * (swk::kInterThreads / 32) * db->scratch_cols_intra) * 32 * (int64_t)sizeof(uint2);
   info->max_len = db->max_len;
   info->device = db->device;
   info->long_threshold = db->long_threshold;
@@ -425,8 +433,19 @@ static int finish_create(sw_db* db) {
   const int64_t n_seqs = db->n_seqs;
   // ---- DP boundary scratch: one slab per resident warp of the persistent kernels ----
   db->scratch_slots = db->num_sms * (swk::kMaxThreads / 32);
-  db->scratch_cols = ((int64_t)db->max_inter_len + swk::kResPerWord) / swk::kResPerWord * swk::kResPerWord + swk::kResPerWord;
+  // Inter-task tiles need one boundary column per subject column (capped: longer
+  // groups go to the intra-task path); the intra-task wavefronts need 2 x ncols
+  // words of the same slab (pass parity).
+  {
+    const int64_t inter = std::min<int64_t>(((int64_t)db->max_inter_len + swk::kResPerWord) / swk::kResPerWord *
+                                            swk::kResPerWord + swk::kResPerWord, swk::kMaxInterCols);
+    const int64_t intra = ((int64_t)db->max_len + 15) / 16 + 8;
+    db->scratch_cols = std::max(inter, intra);
+  }
   CK(cudaMalloc(&db->d_scratch, (size_t)db->scratch_slots * db->scratch_cols * 32 * sizeof(uint2)));
+  db->scratch_cols_intra = ((int64_t)db->max_len + 15) / 16 + 2;   // 2 x max_len words per warp
+  CK(cudaMalloc(&db->d_scratch_intra,
+                (size_t)db->num_sms * (swk::kInterThreads / 32) * db->scratch_cols_intra * 32 * sizeof(uint2)));
 
   // ---- per-search buffers sized by n ----
   const int64_t n1 = std::max<int64_t>(n_seqs, 1);
@@ -453,6 +472,9 @@ static int finish_create(sw_db* db) {
   CK(cudaMemset(db->d_hist, 0, 256 * sizeof(unsigned)));
   CK(cudaMalloc(&db->d_sel, sizeof(swk::SelState)));
   CK(cudaMalloc(&db->d_matrix, 32 * 32));
+  CK(cudaStreamCreateWithFlags(&db->aux, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&db->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&db->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&db->ev_stage, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&db->ev_done, cudaEventDisableTiming));
   for (auto& set : db->ev_ring)
@@ -835,19 +857,21 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   const size_t smem_bytes = smem ? prof_bytes : 0;
   const int grid = db->num_sms;   // one persistent 384-thread CTA per SM
   const int limit16 = 32767 - smax;
-  // groups whose inter-task work would exceed ~1/3 of a warp's average share are
-  // split into pairs for the intra-task wavefront (load balance; DESIGN.md §"Work queue")
-  int n_long = 0;
+  // groups whose inter-task work would exceed ~a warp's average share (or that do
+  // not fit the per-warp boundary slab) are aligned pair by pair by the
+  // intra-task wavefront kernel (load balance)
+  int cut = 0;
   {
-    int64_t cut = 0;   // groups with ncols > cut go intra
+    int64_t c;
     const int64_t n_warps = (int64_t)db->num_sms * (swk::kInterThreads / 32);
-    if (db->long_threshold > 0) cut = db->long_threshold;
-    else if (db->long_threshold == 0) cut = std::max<int64_t>(256, db->sum_len / (64 * std::max<int64_t>(n_warps, 1)));
-    else cut = INT64_MAX;
-    if (const char* e = getenv("SW_LONG_COLS")) cut = atoll(e);
-    const auto it = std::upper_bound(db->group_ncols.begin(), db->group_ncols.end(), (int)std::min<int64_t>(cut, INT32_MAX));
-    n_long = (int)(db->group_ncols.end() - it);
+    if (db->long_threshold > 0) c = db->long_threshold;
+    else if (db->long_threshold == 0) c = std::max<int64_t>(256, db->sum_len / (64 * std::max<int64_t>(n_warps, 1)));
+    else c = INT64_MAX;
+    if (const char* e = getenv("SW_LONG_COLS")) c = atoll(e);
+    cut = (int)std::min<int64_t>(c, db->scratch_cols);
   }
+  const int n_long = (int)(db->group_ncols.end() -
+                           std::upper_bound(db->group_ncols.begin(), db->group_ncols.end(), cut));
   db->last_n_long = n_long;
   const int nb_scan = std::max(1, (n + swk::kScanBlock - 1) / swk::kScanBlock);
   // compaction of a flag byte array into an ascending list of sorted positions
@@ -864,14 +888,33 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   void* kern16 = T == 32 ? inter16_kernel_nt<32>(smem, nt) : T == 48 ? inter16_kernel_nt<48>(smem, nt)
                : inter16_kernel_nt<64>(smem, nt);
   CK(cudaFuncSetAttribute(kern16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
+  const int intra_tr = m_pad <= 256 ? 8 : 16;   // rows per lane of the intra-task wavefront
+  void* kintra = intra_tr == 8 ? (smem ? (void*)swk::k_intra16<8, true> : (void*)swk::k_intra16<8, false>)
+                               : (smem ? (void*)swk::k_intra16<16, true> : (void*)swk::k_intra16<16, false>);
+  CK(cudaFuncSetAttribute(kintra, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
+  // int16x2 pass: the intra-task kernel (long groups, pair items) runs on the aux
+  // stream beside the inter-task kernel (all other groups); both take work
+  // longest-first from their own counters.
   auto launch16 = [&](const uint2* words, const GroupDesc* groups, int n_groups_i, const int* n_groups_dev,
-                      const int* pos_map, int n_long_i, int* counter) -> int {
+                      const int* pos_map, bool any_long, int* counter_inter, int* counter_intra) -> int {
     long long scols = db->scratch_cols;
-    void* kargs[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &n_long_i,
-                     &db->d_prof, (void*)&m_pad, (void*)&stride, &alpha, &beta, (void*)&limit16, &db->d_scratch,
-                     &scols, &counter, &db->d_score_sorted, &db->d_flag16};
-    CK(cudaLaunchKernel(kern16, dim3(grid), dim3(nt), kargs, smem_bytes, st));
+    void* kargs_inter[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &cut,
+                           &db->d_prof, (void*)&m_pad, (void*)&stride, &alpha, &beta, (void*)&limit16, &db->d_scratch,
+                           &scols, &counter_inter, &db->d_score_sorted, &db->d_flag16};
+    long long scols_intra = db->scratch_cols_intra;
+    void* kargs_intra[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &cut,
+                           &db->d_prof, (void*)&m_pad, (void*)&stride, &alpha, &beta, (void*)&limit16,
+                           &db->d_scratch_intra, &scols_intra, &counter_intra, &db->d_score_sorted, &db->d_flag16};
+    if (any_long) {
+      CK(cudaEventRecord(db->ev_fork, st));
+      CK(cudaStreamWaitEvent(db->aux, db->ev_fork, 0));
+      CK(cudaLaunchKernel(kintra, dim3(grid), dim3(swk::kInterThreads), kargs_intra, smem_bytes, db->aux));
+      CK(cudaEventRecord(db->ev_join, db->aux));
+      nl++;
+    }
+    CK(cudaLaunchKernel(kern16, dim3(grid), dim3(nt), kargs_inter, smem_bytes, st));
     nl++;
+    if (any_long) CK(cudaStreamWaitEvent(st, db->ev_join, 0));
     return SW_OK;
   };
   // int8 first stage only when every biased byte fits
@@ -905,10 +948,12 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
                                                                       nmm, db->d_mgroups, db->d_mwords);
       nl += 3;
       CK(cudaGetLastError());
-      rc = launch16(db->d_mwords, db->d_mgroups, nmm, db->d_cnt + 2, db->d_list8, 0, db->d_counters + 4);
+      rc = launch16(db->d_mwords, db->d_mgroups, nmm, db->d_cnt + 2, db->d_list8, true, db->d_counters + 4,
+                    db->d_counters + 7);
       if (rc) return rc;
     } else if (db->first_stage != 32) {
-      int rc = launch16(db->d_words, db->d_groups, (int)db->n_groups, nullptr, nullptr, n_long, db->d_counters + 0);
+      int rc = launch16(db->d_words, db->d_groups, (int)db->n_groups, nullptr, nullptr, n_long > 0, db->d_counters + 0,
+                        db->d_counters + 6);
       if (rc) return rc;
       CK(cudaEventRecord(ev[2], st));
     } else {

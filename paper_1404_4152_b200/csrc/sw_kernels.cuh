@@ -50,6 +50,18 @@ __host__ __device__ constexpr uint32_t sel_one(int rr) {
   return (uint32_t)(rr | ((rr | 8) << 4) | ((rr | 8) << 8) | ((rr | 8) << 12));
 }
 
+// Dynamic shared memory holds the query profile when it fits (SMEM = true).
+// Re-deriving the base inside non-inlined helpers keeps their loads LDS.
+template <bool SMEM>
+__device__ __forceinline__ const int8_t* prof_base(const int8_t* gprof) {
+  if constexpr (SMEM) {
+    extern __shared__ __align__(16) int8_t dyn_smem[];
+    return dyn_smem;
+  } else {
+    return gprof;
+  }
+}
+
 __device__ __forceinline__ uint32_t pack2(int v) {
   const uint32_t h = (uint32_t)v & 0xffffu;
   return h | (h << 16);
@@ -283,6 +295,21 @@ __device__ __forceinline__ void tile16_rem(int rem, const uint2* gw, int ncols, 
   }
 }
 
+// One 64-subject group, all query tiles (inter-task).  Not inlined, so the
+// register-hungry tile loop is allocated apart from the persistent queue logic.
+template <int T, bool SMEM>
+__device__ __forceinline__ uint32_t inter_group16(const uint2* __restrict__ gw, int ncols, const int8_t* __restrict__ gprof,
+                                               int stride, int m_pad, uint2* __restrict__ bnd, uint32_t na2,
+                                               uint32_t nb2, int lane) {
+  const int8_t* prof = prof_base<SMEM>(gprof);
+  const int nfull = m_pad / T, rem = m_pad - nfull * T;
+  uint32_t hmax = 0u;
+  for (int t = 0; t < nfull; t++)
+    tile16<T>(gw, ncols, prof, stride, t * T, bnd, t == 0, t == nfull - 1 && rem == 0, na2, nb2, hmax, lane);
+  if (rem) tile16_rem<T>(rem, gw, ncols, prof, stride, nfull * T, bnd, nfull == 0, na2, nb2, hmax, lane);
+  return hmax;
+}
+
 // ---------------------------------------------------------------------------
 // Intra-task wavefront for ONE pair of long subjects per warp (north star (c);
 // the role of the paper's intra-sequence model, with a
@@ -292,11 +319,12 @@ __device__ __forceinline__ void tile16_rem(int rem, const uint2* gw, int ncols, 
 // last active lane's output row is kept in gbnd for the next pass.
 // Returns this lane's running max (to be reduced over the warp).
 // ---------------------------------------------------------------------------
-template <int TR>
+template <int TR, bool SMEM>
 __device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, int ncols,
-                                                 const int8_t* __restrict__ prof, int stride, int m_pad,
+                                                 const int8_t* __restrict__ gprof, int stride, int m_pad,
                                                  uint2* __restrict__ gbnd, long long gstride,
                                                  uint32_t na2, uint32_t nb2, int lane) {
+  const int8_t* prof = prof_base<SMEM>(gprof);
   uint32_t hmax = 0u;
   const int nwords = (ncols + kResPerWord - 1) / kResPerWord;
   int pass = 0;
@@ -305,41 +333,59 @@ __device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, i
     const bool first = base == 0, last = base + 32 * TR >= m_pad;
     const uint2* gin = gbnd + (long long)(pass & 1) * gstride;          // written by the previous pass
     uint2* gout = gbnd + (long long)((pass + 1) & 1) * gstride;
-    const int i0 = base + lane * TR;
+    const int8_t* pr = prof + base + lane * TR;
     uint32_t D[TR], F[TR];
 #pragma unroll
     for (int r = 0; r < TR; r++) { D[r] = 0u; F[r] = 0u; }
     uint32_t e_out = 0u, h_out = 0u, r_out = 0u;
-    // lane 0's cursor over the pair's residues (uncoalesced single-lane reads)
-    ResCursor rc;
-    rc.init(pw, nwords);
-    uint2 gnext = make_uint2(0u, 0u);
-    if (!first && lane == 0) gnext = gin[0];
+    // Lane 0's per-step inputs (the residue pair of column s+1 and, after the
+    // first pass, the previous pass's boundary of column s) are fetched by all
+    // lanes for 32 steps at a time, one block ahead, and handed to lane 0 by
+    // SHFL -- no load latency on the wavefront's critical step.
+    auto fetch = [&](int sb, uint32_t& rp, uint2& gv) {
+      const int c = sb + 1 + lane;                                      // residue column for step sb + lane
+      const uint2 w = res_word(pw, c, nwords);
+      const int sh = res_shift(c);
+      rp = ((w.x >> sh) & 31u) | (((w.y >> sh) & 31u) << 5);
+      const int gc = sb + lane;                                         // boundary column for step sb + lane
+      gv = (!first && gc >= 0 && gc < ncols) ? gin[gc] : make_uint2(0u, 0u);
+    };
+    const int nsteps = ncols + nact;                                    // steps s = -1 .. ncols + nact - 2
+    uint32_t rp_cur, rp_nxt;
+    uint2 gv_cur, gv_nxt;
+    fetch(-1, rp_cur, gv_cur);
+    fetch(31, rp_nxt, gv_nxt);
     __syncwarp();
-    for (int s = -1; s < ncols + nact - 1; s++) {
-      uint32_t e_in = __shfl_up_sync(0xffffffffu, e_out, 1);
-      uint32_t h_in = __shfl_up_sync(0xffffffffu, h_out, 1);
-      uint32_t r_in = __shfl_up_sync(0xffffffffu, r_out, 1);
-      const int j = s - lane;
-      if (lane == 0) {
-        r_in = rc.lo() | (rc.hi() << 5);                             // residues of column j+1
-        rc.next();
-        if (first || j < 0) { e_in = 0u; h_in = 0u; }
-        else {
-          e_in = gnext.x;
-          h_in = gnext.y;
-          gnext = (j + 1 < ncols) ? gin[j + 1] : make_uint2(0u, 0u);
+    for (int sb = -1; sb < nsteps - 1; sb += 32) {
+#pragma unroll 1
+      for (int t = 0; t < 32; t++) {
+        const int s = sb + t;
+        if (s >= nsteps - 1) break;
+        uint32_t e_in = __shfl_up_sync(0xffffffffu, e_out, 1);
+        uint32_t h_in = __shfl_up_sync(0xffffffffu, h_out, 1);
+        uint32_t r_in = __shfl_up_sync(0xffffffffu, r_out, 1);
+        const uint32_t r0 = __shfl_sync(0xffffffffu, rp_cur, t);
+        const uint32_t g0x = __shfl_sync(0xffffffffu, gv_cur.x, t);
+        const uint32_t g0y = __shfl_sync(0xffffffffu, gv_cur.y, t);
+        const int j = s - lane;
+        if (lane == 0) {
+          r_in = r0;                                                    // residues of column j+1
+          e_in = g0x;                                                   // E(base, j), H(base-1, j) (0 on pass 0 / j < 0)
+          h_in = g0y;
+        }
+        if (lane < nact && j >= -1 && j < ncols) {
+          uint32_t e = e_in;
+          const uint32_t hl = col16<TR>(D, F, e, h_in, pr + (r_in & 31u) * stride, pr + (r_in >> 5) * stride,
+                                        na2, nb2, hmax);
+          e_out = e;
+          h_out = hl;
+          r_out = r_in;
+          if (!last && lane == nact - 1 && j >= 0) gout[j] = make_uint2(e, hl);
         }
       }
-      if (lane < nact && j >= -1 && j < ncols) {
-        uint32_t e = e_in;
-        const uint32_t hl = col16<TR>(D, F, e, h_in, prof + (r_in & 31u) * stride + i0,
-                                      prof + (r_in >> 5) * stride + i0, na2, nb2, hmax);
-        e_out = e;
-        h_out = hl;
-        r_out = r_in;
-        if (!last && lane == nact - 1 && j >= 0) gout[j] = make_uint2(e, hl);
-      }
+      rp_cur = rp_nxt;
+      gv_cur = gv_nxt;
+      fetch(sb + 64, rp_nxt, gv_nxt);
     }
     __syncwarp();
   }
@@ -380,55 +426,87 @@ __device__ __forceinline__ void emit_pair(uint32_t hmax, int g, int slot, int co
 
 constexpr int kIntraRows = 16;   // rows per lane in the intra-task wavefront
 constexpr int kIntra32Cols = 512; // int32 reruns: longer subjects go one per warp (wavefront)
+constexpr int kMaxInterCols = 6144; // boundary-slab columns per warp; longer groups go intra-task
 
+// First group (ascending ncols) whose ncols exceeds `cut`: groups at and above it
+// go to the intra-task kernel.  Same answer in both kernels.
+__device__ __forceinline__ int split_groups(const GroupDesc* __restrict__ groups, int n_groups, int cut) {
+  int lo = 0, hi = n_groups;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (groups[mid].ncols > cut) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+// Inter-task pass over groups [0, split): whole 64-subject groups, longest first.
 template <int T, bool SMEM, int NT>
 __global__ void __launch_bounds__(NT, 1)
 k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
-          const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int n_long,
+          const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
           int* __restrict__ score_sorted, uint8_t* __restrict__ flag) {
   extern __shared__ __align__(16) int8_t sprof[];
+  __shared__ int s_split;
   if (n_groups_dev) n_groups = *n_groups_dev;   // mini-group layout of a rerun: size known on device only
-  if (n_groups <= 0) return;
-  const int8_t* prof = gprof;
-  if (SMEM) {
-    load_profile_smem(sprof, gprof, stride);
-    prof = sprof;
-  }
+  if (threadIdx.x == 0) s_split = split_groups(groups, n_groups, cut);
+  __syncthreads();
+  const int n_items = s_split;
+  if (n_items <= 0) return;
+  if (SMEM) load_profile_smem(sprof, gprof, stride);
   const int lane = threadIdx.x & 31;
-  const long long wslot = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  uint2* bnd = scratch + wslot * scratch_cols * 32;
+  uint2* bnd = scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
   const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
-  const int nfull = m_pad / T, rem = m_pad - nfull * T;
-  const int n_long_items = n_long * 32;
-  const int n_items = n_long_items + (n_groups - n_long);
   for (;;) {
     int item = 0;
     if (lane == 0) item = atomicAdd(counter, 1);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
-    if (item < n_long_items) {
-      const int g = n_groups - 1 - item / 32;
-      const int p = 31 - item % 32;
-      const GroupDesc gd = groups[g];
-      if (2 * p >= gd.count) continue;
-      uint32_t hm = intra_pair16<kIntraRows>(words + gd.base + p, gd.ncols, prof, stride, m_pad, bnd,
-                                             scratch_cols * 16, na2, nb2, lane);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) hm = __vmaxs2(hm, __shfl_xor_sync(0xffffffffu, hm, o));
-      if (lane == 0) emit_pair(hm, g, 2 * p, gd.count, limit, pos_map, score_sorted, flag);
-      continue;
-    }
-    const int g = (n_groups - n_long) - 1 - (item - n_long_items);
+    const int g = n_items - 1 - item;
     const GroupDesc gd = groups[g];
-    const uint2* gw = words + gd.base;
-    uint32_t hmax = 0u;
-    for (int t = 0; t < nfull; t++)
-      tile16<T>(gw, gd.ncols, prof, stride, t * T, bnd, t == 0, t == nfull - 1 && rem == 0,
-                na2, nb2, hmax, lane);
-    if (rem) tile16_rem<T>(rem, gw, gd.ncols, prof, stride, nfull * T, bnd, nfull == 0, na2, nb2, hmax, lane);
+    const uint32_t hmax = inter_group16<T, SMEM>(words + gd.base, gd.ncols, gprof, stride, m_pad, bnd, na2, nb2, lane);
     emit_pair(hmax, g, 2 * lane, gd.count, limit, pos_map, score_sorted, flag);
+  }
+}
+
+// Intra-task pass over groups [split, n_groups): one subject PAIR per work item,
+// longest first, aligned by the lane wavefront.  A kernel of its own (own
+// register allocation), launched on a second stream beside k_inter16.
+template <int TR, bool SMEM>
+__global__ void __launch_bounds__(kInterThreads, 1)
+k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
+          const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
+          const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
+          uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
+          int* __restrict__ score_sorted, uint8_t* __restrict__ flag) {
+  extern __shared__ __align__(16) int8_t sprof[];
+  __shared__ int s_split;
+  if (n_groups_dev) n_groups = *n_groups_dev;
+  if (threadIdx.x == 0) s_split = split_groups(groups, n_groups, cut);
+  __syncthreads();
+  const int split = s_split;
+  const int n_items = (n_groups - split) * 32;
+  if (n_items <= 0) return;
+  if (SMEM) load_profile_smem(sprof, gprof, stride);
+  const int lane = threadIdx.x & 31;
+  uint2* bnd = scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
+  const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(counter, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    const int g = n_groups - 1 - item / 32;
+    const int p = 31 - item % 32;
+    const GroupDesc gd = groups[g];
+    if (2 * p >= gd.count) continue;
+    uint32_t hm = intra_pair16<TR, SMEM>(words + gd.base + p, gd.ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
+                                         na2, nb2, lane);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hm = __vmaxs2(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+    if (lane == 0) emit_pair(hm, g, 2 * p, gd.count, limit, pos_map, score_sorted, flag);
   }
 }
 
@@ -561,6 +639,14 @@ k_inter8(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, 
     d1.count = 0;
     if (g1 < n_groups) d1 = groups[g1];
     const int ncols = max(d0.ncols, d1.ncols);
+    if (ncols > scratch_cols) {            // too long for the boundary slab: straight to the int16 rerun
+      for (int b = 0; b < 4; b++) {
+        const GroupDesc& d = b < 2 ? d0 : d1;
+        const int slot = 2 * lane + (b & 1);
+        if (slot < d.count) flag[(b < 2 ? g0 : g1) * kGroup + slot] = 1;
+      }
+      continue;
+    }
     const int nw0 = (d0.ncols + kResPerWord - 1) / kResPerWord, nw1 = (d1.ncols + kResPerWord - 1) / kResPerWord;
     const uint2* gw0 = words + d0.base;
     const uint2* gw1 = words + d1.base;
@@ -770,12 +856,12 @@ k_list32(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   // A sorted list (reruns) ends with its longest subjects: entries longer than
   // kIntra32Cols are taken one per warp by the intra-task wavefront (first, as
   // the longest work), the rest 32 per warp, one per lane.
-  int n_short = n;
-  if (list) {
-    int lo = 0, hi = n;                               // first entry with len > cut
+  int n_short;
+  {
+    int lo = 0, hi = n;                               // first entry with len > cut (lists are ascending)
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (len_sorted[list[mid]] > kIntra32Cols) hi = mid;
+      if (len_sorted[list ? list[mid] : mid] > kIntra32Cols) hi = mid;
       else lo = mid + 1;
     }
     n_short = lo;
@@ -788,7 +874,7 @@ k_list32(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
     if (item < n_long) {
-      const int pos = list[n - 1 - item];
+      const int pos = list ? list[n - 1 - item] : n - 1 - item;
       const int len = len_sorted[pos];
       const int slot = pos & (kGroup - 1);
       const uint32_t* wp = reinterpret_cast<const uint32_t*>(words) + 2 * (groups[pos / kGroup].base + (slot >> 1)) + (slot & 1);
@@ -943,6 +1029,13 @@ k_multi16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     const int half = 1 - (item & 1);
     const GroupDesc gd = groups[g];
     const int slot = 2 * lane + half;
+    if (gd.ncols > scratch_cols) {         // too long for the boundary slab: both queries go to the int32 rerun
+      if (slot < gd.count) {
+        flag_a[g * kGroup + slot] = 1;
+        flag_b[g * kGroup + slot] = 1;
+      }
+      continue;
+    }
     const uint32_t* wp = reinterpret_cast<const uint32_t*>(words) + 2 * (gd.base + lane) + half;
     const int nwords = (gd.ncols + kResPerWord - 1) / kResPerWord;
     uint32_t hmax = 0u;

@@ -309,3 +309,19 @@ def test_persistent_index_roundtrip(tmp_path):
         assert np.array_equal(r0.topk_ids, r1.topk_ids) and np.array_equal(r0.topk_scores, r1.topk_scores)
     ref = oracle.db_scores(q, db, B62, 2, 12)
     assert np.array_equal(r1.scores, ref)
+
+
+@pytest.mark.parametrize("first_stage", [16, 8, 32])
+def test_very_long_subjects_exceeding_boundary_slab(first_stage):
+    """Subjects longer than the per-warp boundary slab (6,144 columns) are always
+    aligned intra-task (or rerun), in every stage; scores stay exact."""
+    rng = np.random.default_rng(91)
+    lens = np.concatenate([rng.integers(1, 300, size=200), [7000, 9000, 20000, 6145, 6144]])
+    db = random_db(91, lens)
+    q = _query(700, 91)
+    db.residues[db.offsets[202]:db.offsets[202] + 700] = q          # one strong hit inside the 20,000-long subject
+    _check(db, q, B62, 2, 12, first_stage=first_stage, long_threshold=-1)
+    with sw.Database.from_synth(db, device=0) as g:
+        r = g.search_batch([q, _query(300, 92)], B62, 2, 12, k=5)
+    for i, qq in enumerate([q, _query(300, 92)]):
+        assert np.array_equal(r.scores[i], oracle.db_scores(qq, db, B62, 2, 12))
