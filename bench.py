@@ -190,9 +190,10 @@ def load_ncu_traffic():
     try:
         with open(paths[-1]) as f:
             d = json.load(f)
-        return {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"), "source": os.path.relpath(paths[-1], ROOT)}
+        return {"traffic": d.get("dram_bytes_per_launch"), "traffic_unit": "B/launch (ncu dram read+write)",
+                "traffic_source": os.path.relpath(paths[-1], ROOT)}
     except Exception:
-        return None
+        return {"traffic": None}
 
 
 def main():
@@ -332,7 +333,7 @@ def main():
                          "kernel": "k_inter16 (int16x2 DPX first pass)",
                          "kernel_ms": round(ms_inter, 4), "kernel_share_of_step": round(ms_inter / ms_step, 4),
                          "peak_basis": "148 SM x 1965 MHz x 64 DPX lanes/clk/SM (measured) / 1.75 alu-pipe ops per cell",
-                         "traffic": load_ncu_traffic()},
+                         **load_ncu_traffic()},
             "clocks": clk,
             "gpu_launches": int(launches),
             "e2e": e2e,

@@ -106,8 +106,6 @@ struct sw_db {
   int device = 0;
   int num_sms = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t aux = nullptr;     // intra-task kernel beside the inter-task one
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::mutex mu;
   int first_stage = 16;
   int long_threshold = -1;
@@ -224,9 +222,6 @@ static void free_db(sw_db* db) {
   for (auto& set : db->ev_ring)
     for (auto& e : set)
       if (e) cudaEventDestroy(e);
-  if (db->ev_fork) cudaEventDestroy(db->ev_fork);
-  if (db->ev_join) cudaEventDestroy(db->ev_join);
-  if (db->aux) cudaStreamDestroy(db->aux);
   if (db->stream) cudaStreamDestroy(db->stream);
   delete db;
 }
@@ -472,9 +467,6 @@ static int finish_create(sw_db* db) {
   CK(cudaMemset(db->d_hist, 0, 256 * sizeof(unsigned)));
   CK(cudaMalloc(&db->d_sel, sizeof(swk::SelState)));
   CK(cudaMalloc(&db->d_matrix, 32 * 32));
-  CK(cudaStreamCreateWithFlags(&db->aux, cudaStreamNonBlocking));
-  CK(cudaEventCreateWithFlags(&db->ev_fork, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&db->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&db->ev_stage, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&db->ev_done, cudaEventDisableTiming));
   for (auto& set : db->ev_ring)
@@ -892,9 +884,13 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   void* kintra = intra_tr == 8 ? (smem ? (void*)swk::k_intra16<8, true> : (void*)swk::k_intra16<8, false>)
                                : (smem ? (void*)swk::k_intra16<16, true> : (void*)swk::k_intra16<16, false>);
   CK(cudaFuncSetAttribute(kintra, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
-  // int16x2 pass: the intra-task kernel (long groups, pair items) runs on the aux
-  // stream beside the inter-task kernel (all other groups); both take work
-  // longest-first from their own counters.
+  // int16x2 pass: the intra-task kernel (long groups, pair items) is launched
+  // first and at once lets the inter-task kernel (all other groups) start beside
+  // it (programmatic dependent launch on the same stream): its few CTAs reach
+  // the SMs first, the persistent inter-task CTAs fill the rest, and the
+  // inter-task kernel's last instruction waits for the intra-task grid, so
+  // everything after it on the stream sees both.  Both take work longest-first
+  // from their own counters.
   auto launch16 = [&](const uint2* words, const GroupDesc* groups, int n_groups_i, const int* n_groups_dev,
                       const int* pos_map, bool any_long, int* counter_inter, int* counter_intra) -> int {
     long long scols = db->scratch_cols;
@@ -905,16 +901,26 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
     void* kargs_intra[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &cut,
                            &db->d_prof, (void*)&m_pad, (void*)&stride, &alpha, &beta, (void*)&limit16,
                            &db->d_scratch_intra, &scols_intra, &counter_intra, &db->d_score_sorted, &db->d_flag16};
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.stream = st;
     if (any_long) {
-      CK(cudaEventRecord(db->ev_fork, st));
-      CK(cudaStreamWaitEvent(db->aux, db->ev_fork, 0));
-      CK(cudaLaunchKernel(kintra, dim3(grid), dim3(swk::kInterThreads), kargs_intra, smem_bytes, db->aux));
-      CK(cudaEventRecord(db->ev_join, db->aux));
+      // only as many CTAs as the pair items need (12 warps each): idle CTAs would
+      // hold SMs the inter-task kernel could use
+      const int64_t items = (int64_t)(n_groups_dev ? n_groups_i : n_long) * 32;
+      const int grid_intra = (int)std::max<int64_t>(1, std::min<int64_t>(grid, (items + 11) / 12));
+      CK(cudaLaunchKernel(kintra, dim3(grid_intra), dim3(swk::kInterThreads), kargs_intra, smem_bytes, st));
       nl++;
+      cfg.attrs = pdl;
+      cfg.numAttrs = 1;
     }
-    CK(cudaLaunchKernel(kern16, dim3(grid), dim3(nt), kargs_inter, smem_bytes, st));
+    cfg.gridDim = dim3(grid);
+    CK(cudaLaunchKernelExC(&cfg, kern16, kargs_inter));
     nl++;
-    if (any_long) CK(cudaStreamWaitEvent(st, db->ev_join, 0));
     return SW_OK;
   };
   // int8 first stage only when every biased byte fits

@@ -454,7 +454,10 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   if (threadIdx.x == 0) s_split = split_groups(groups, n_groups, cut);
   __syncthreads();
   const int n_items = s_split;
-  if (n_items <= 0) return;
+  if (n_items <= 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   if (SMEM) load_profile_smem(sprof, gprof, stride);
   const int lane = threadIdx.x & 31;
   uint2* bnd = scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
@@ -469,6 +472,10 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     const uint32_t hmax = inter_group16<T, SMEM>(words + gd.base, gd.ncols, gprof, stride, m_pad, bnd, na2, nb2, lane);
     emit_pair(hmax, g, 2 * lane, gd.count, limit, pos_map, score_sorted, flag);
   }
+  // Launched as the programmatic dependent of k_intra16 (same stream): do not
+  // retire before that grid has completed, so the stream's later work sees its
+  // scores.  A no-op when there is no primary grid.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // Intra-task pass over groups [split, n_groups): one subject PAIR per work item,
@@ -481,6 +488,9 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
           int* __restrict__ score_sorted, uint8_t* __restrict__ flag) {
+  // The inter-task kernel may start beside this one (programmatic dependent
+  // launch): it only reads what was complete before this grid started.
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ __align__(16) int8_t sprof[];
   __shared__ int s_split;
   if (n_groups_dev) n_groups = *n_groups_dev;
