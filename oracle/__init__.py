@@ -10,7 +10,10 @@ swdata/ only.
 * `sw_full`: Gotoh full matrix with -inf boundaries (pins reading R2).
 * `topk`: stage (iv) "sort all alignment scores in descending order"
    by a full sort, tie-break id ascending (reading R7).
-* `brute.brute_force`: enumeration of every local alignment (tiny inputs).
+* `sw_align`: one optimal local alignment by full-matrix traceback with the
+  deterministic tie rules of DESIGN.md R17-R19 (f3).
+* `brute.brute_force`: enumeration of every local alignment (tiny inputs);
+  `brute.optimal_alignments`: the set of all optimal ones.
 
 Pinned by tests/test_oracle.py (-m "not gpu"); no function is parity-unpinned.
 """
@@ -49,6 +52,8 @@ def lib():
         L.oracle_scores.restype = ctypes.c_int
         L.oracle_topk.argtypes = [P, P, i64, i32, P, P]
         L.oracle_topk.restype = ctypes.c_int
+        L.oracle_sw_align.argtypes = [P, i32, P, i32, P, i32, i32, P, ctypes.c_char_p]
+        L.oracle_sw_align.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -123,3 +128,18 @@ def topk(scores_, k: int, ids=None):
     if lib().oracle_topk(sc.ctypes.data, idp, sc.size, k, oi.ctypes.data, os_.ctypes.data) != 0:
         raise MemoryError("oracle_topk")
     return oi, os_
+
+
+def sw_align(q, s, M, alpha: int, beta: int) -> dict:
+    """One optimal local alignment (full-matrix traceback, sw_oracle.c).
+    Returns {score, q_begin, q_end, s_begin, s_end, ops} (0-based, half-open;
+    ops over 'M' / 'I' (query residue vs gap) / 'D' (subject residue vs gap))."""
+    q, s, M = _u8(q), _u8(s), _m32(M)
+    out = np.zeros(6, dtype=np.int32)
+    buf = ctypes.create_string_buffer(q.size + s.size + 1)
+    rc = lib().oracle_sw_align(q.ctypes.data, q.size, s.ctypes.data, s.size, M.ctypes.data, alpha, beta,
+                               out.ctypes.data, buf)
+    if rc != 0:
+        raise MemoryError("oracle_sw_align")
+    return {"score": int(out[0]), "q_begin": int(out[1]), "q_end": int(out[2]), "s_begin": int(out[3]),
+            "s_end": int(out[4]), "ops": buf.raw[:int(out[5])].decode()}

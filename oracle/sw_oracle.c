@@ -164,3 +164,73 @@ int oracle_topk(const int32_t* scores, const int64_t* ids, int64_t n, int32_t k,
   free(h);
   return 0;
 }
+
+/* ---- f3: traceback of one optimal local alignment (the
+ * paper leaves alignment retrieval as future work).  Full
+ * (m+1) x (n+1) matrices of Eq. 1 as printed, then a walk back from the end
+ * cell.  Deterministic readings (R17-R19):
+ *   end cell : the maximal H; ties -> smallest subject position j, then
+ *              smallest query position i;
+ *   H(i,j)   : H == 0 stops the walk; else H == diagonal term -> 'M';
+ *              else H == E(i,j) -> vertical gap; else horizontal gap;
+ *   E(i,j)   : extend (from E(i-1,j)) iff E(i-1,j)-alpha > H(i-1,j)-beta,
+ *              otherwise open (from H(i-1,j)); F likewise along j.
+ * Ops, SAM convention with the query as the read: 'M' = query residue
+ * against subject residue, 'I' = query residue against a gap (E, consumes i),
+ * 'D' = subject residue against a gap (F, consumes j).
+ * out[0] score, out[1] q_begin, out[2] q_end, out[3] s_begin, out[4] s_end
+ * (0-based, half-open; all 0 for the empty alignment of score 0), out[5] the
+ * number of ops written to ops[] (capacity >= m + n).  Returns 0, or -1 if a
+ * buffer cannot be allocated. */
+int oracle_sw_align(const uint8_t* q, int32_t m, const uint8_t* s, int32_t n, const int8_t* M,
+                    int32_t alpha, int32_t beta, int32_t* out, char* ops) {
+  for (int k = 0; k < 6; k++) out[k] = 0;
+  if (m <= 0 || n <= 0) return 0;
+  size_t W = (size_t)n + 1, sz = ((size_t)m + 1) * W;
+  int32_t* H = (int32_t*)calloc(sz, sizeof(int32_t));
+  int32_t* E = (int32_t*)calloc(sz, sizeof(int32_t));   /* E(0,j) = 0 as printed */
+  int32_t* F = (int32_t*)calloc(sz, sizeof(int32_t));   /* F(i,0) = 0 as printed */
+  int32_t* G = (int32_t*)calloc(sz, sizeof(int32_t));   /* the diagonal term H(i-1,j-1) + fsbt */
+  char* rev = (char*)malloc((size_t)m + (size_t)n + 1);
+  if (!H || !E || !F || !G || !rev) { free(H); free(E); free(F); free(G); free(rev); return -1; }
+  int32_t best = 0, bi = 0, bj = 0;
+  for (int32_t i = 1; i <= m; i++)
+    for (int32_t j = 1; j <= n; j++) {
+      size_t c = (size_t)i * W + j, up = c - W, lf = c - 1, dg = up - 1;
+      E[c] = max2(E[up] - alpha, H[up] - beta);
+      F[c] = max2(F[lf] - alpha, H[lf] - beta);
+      G[c] = H[dg] + M[32 * q[i - 1] + s[j - 1]];
+      H[c] = max2(max2(0, G[c]), max2(E[c], F[c]));
+    }
+  /* end cell: scan columns in order, rows in order, keep the first maximum */
+  for (int32_t j = 1; j <= n; j++)
+    for (int32_t i = 1; i <= m; i++)
+      if (H[(size_t)i * W + j] > best) { best = H[(size_t)i * W + j]; bi = i; bj = j; }
+  out[0] = best;
+  if (best == 0) { free(H); free(E); free(F); free(G); free(rev); return 0; }
+  int32_t i = bi, j = bj, nops = 0;
+  int state = 0;                                  /* 0 = H, 1 = E (vertical), 2 = F (horizontal) */
+  for (;;) {
+    size_t c = (size_t)i * W + j;
+    if (state == 0) {
+      if (i == 0 || j == 0 || H[c] == 0) break;
+      if (H[c] == G[c]) { rev[nops++] = 'M'; i--; j--; }
+      else if (H[c] == E[c]) state = 1;
+      else state = 2;
+    } else if (state == 1) {
+      const int ext = E[c - W] - alpha > H[c - W] - beta;
+      rev[nops++] = 'I';
+      i--;
+      state = ext ? 1 : 0;
+    } else {
+      const int ext = F[c - 1] - alpha > H[c - 1] - beta;
+      rev[nops++] = 'D';
+      j--;
+      state = ext ? 2 : 0;
+    }
+  }
+  out[1] = i; out[2] = bi; out[3] = j; out[4] = bj; out[5] = nops;
+  for (int32_t k = 0; k < nops; k++) ops[k] = rev[nops - 1 - k];
+  free(H); free(E); free(F); free(G); free(rev);
+  return 0;
+}
