@@ -175,6 +175,42 @@ int sw_search_batch(sw_db* db, const uint8_t* queries, const int64_t* qoffsets, 
                     int32_t* scores, int64_t* topk_ids, int32_t* topk_scores, sw_stats* stats);
 
 /*
+ * Traceback of optimal local alignments for chosen subjects (SURVEY.md §8(f)
+ * f3; "alignment retrieval" is the paper's future work).  For
+ * each subject the device fills Eq. 1 over the whole query x subject matrix in
+ * int32 with a 4-bit direction code per cell, then walks back from the end
+ * cell.  Deterministic choices (R17-R19): the end cell is the
+ * maximal H with the smallest subject position, then the smallest query
+ * position; on the walk H prefers diagonal, then E, then F; a gap extends only
+ * if that is strictly better than opening.  score equals sw_search's score.
+ *   query/matrix/alpha/beta  as sw_search
+ *   subjects     host int64[n]: INPUT indices (0 .. n_seqs-1), repeats allowed
+ *   out          host sw_alignment[n]
+ *   ops          host buffer; alignment t's ops start at out[t].ops_offset and
+ *                are out[t].n_ops bytes of 'M' (query residue vs subject residue),
+ *                'I' (query residue vs gap) and 'D' (subject residue vs gap),
+ *                in alignment order (SAM convention, the query as the read)
+ *   ops_cap      bytes of ops; must be >= sum over t of (qlen + length of
+ *                subject t), else SW_EINVAL (the message states the need)
+ * Coordinates are 0-based and half-open; a score-0 alignment is empty (all 0).
+ * Device workspace: qlen/2 bytes per cell of the matrices aligned at once,
+ * batched under ~1 GiB (a single larger matrix is allocated alone).
+ * Blocking; host buffers.
+ */
+typedef struct sw_alignment {
+  int64_t subject;        /* input index */
+  int32_t score;
+  int32_t q_begin, q_end; /* query residues [q_begin, q_end) */
+  int32_t s_begin, s_end; /* subject residues [s_begin, s_end) */
+  int32_t n_ops;
+  int32_t reserved;
+  int64_t ops_offset;
+} sw_alignment;
+
+int sw_align(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix, int32_t alpha,
+             int32_t beta, const int64_t* subjects, int32_t n, sw_alignment* out, char* ops, int64_t ops_cap);
+
+/*
  * Merge n_lists top-k lists (host; e.g. one per GPU after an all-gather) into
  * the global top-k by (score desc, id asc).  Entries with id < 0 are ignored.
  *   ids/scores   host, n_lists * k_in entries (list-major)

@@ -55,9 +55,15 @@ class sw_db_info(ctypes.Structure):
                 ("long_threshold", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
+class sw_alignment(ctypes.Structure):
+    _fields_ = [("subject", ctypes.c_int64), ("score", ctypes.c_int32), ("q_begin", ctypes.c_int32),
+                ("q_end", ctypes.c_int32), ("s_begin", ctypes.c_int32), ("s_end", ctypes.c_int32),
+                ("n_ops", ctypes.c_int32), ("reserved", ctypes.c_int32), ("ops_offset", ctypes.c_int64)]
+
+
 # Every symbol include/swsearch.h declares (tests check the .so exports all of them).
 EXPORTS = ("sw_opts_default", "sw_db_create", "sw_search", "sw_search_async", "sw_search_batch", "sw_merge_topk",
-           "sw_db_get_info", "sw_db_stage_times", "sw_db_save", "sw_db_load", "sw_db_destroy", "sw_strerror",
+           "sw_db_get_info", "sw_db_stage_times", "sw_align", "sw_db_save", "sw_db_load", "sw_db_destroy", "sw_strerror",
            "sw_last_error")
 
 _lib = None
@@ -81,6 +87,8 @@ def lib() -> ctypes.CDLL:
         L.sw_search_async.restype = ctypes.c_int
         L.sw_search_batch.argtypes = [P, P, P, P, i32, P, i32, i32, i32, P, P, P, ctypes.POINTER(sw_stats)]
         L.sw_search_batch.restype = ctypes.c_int
+        L.sw_align.argtypes = [P, P, i32, P, i32, i32, P, i32, ctypes.POINTER(sw_alignment), P, i64]
+        L.sw_align.restype = ctypes.c_int
         L.sw_merge_topk.argtypes = [P, P, i32, i32, i32, P, P]
         L.sw_merge_topk.restype = ctypes.c_int
         L.sw_db_get_info.argtypes = [P, ctypes.POINTER(sw_db_info)]
@@ -144,6 +152,7 @@ class Database:
                               None if gids is None else _ptr(gids), ctypes.byref(o), ctypes.byref(h)))
         self._h = h
         self.n_seqs = int(lens.size)
+        self._lengths = lens.copy()        # sizes the ops buffer of align()
 
     @classmethod
     def from_synth(cls, db, **kw) -> "Database":
@@ -160,6 +169,7 @@ class Database:
         _check(L.sw_db_load(os.fsencode(path), ctypes.byref(o), ctypes.byref(h)))
         self = cls.__new__(cls)
         self._h = h
+        self._lengths = None
         self.n_seqs = self.info()["n_seqs"]
         return self
 
@@ -218,6 +228,31 @@ class Database:
         d = st.as_dict()
         d["pairs"] = st.reserved[0]
         return SearchResult(sc, ti, ts, d)
+
+    def align(self, query, matrix, alpha: int, beta: int, subjects) -> list:
+        """sw_align: one optimal local alignment per subject (input indices).
+        Returns dicts {subject, score, q_begin, q_end, s_begin, s_end, ops}
+        (0-based half-open ranges; ops over 'M', 'I' = query residue vs gap,
+        'D' = subject residue vs gap)."""
+        q = np.ascontiguousarray(query, dtype=np.uint8)
+        M = np.ascontiguousarray(matrix, dtype=np.int8)
+        idx = np.ascontiguousarray(np.atleast_1d(subjects), dtype=np.int64)
+        n = idx.size
+        if n == 0:
+            return []
+        ok = getattr(self, "_lengths", None) is not None and idx.min() >= 0 and idx.max() < self.n_seqs
+        lens = self._lengths[idx] if ok else None      # out-of-range ids: the library reports them
+        cap = int(n * q.size + (lens.sum() if lens is not None else n * (self.info()["max_len"])))
+        out = (sw_alignment * n)()
+        buf = ctypes.create_string_buffer(max(cap, 1))
+        _check(lib().sw_align(self._h, _ptr(q), q.size, _ptr(M), alpha, beta, _ptr(idx), n, out, buf, cap))
+        raw = buf.raw
+        res = []
+        for a in out:
+            res.append({"subject": a.subject, "score": a.score, "q_begin": a.q_begin, "q_end": a.q_end,
+                        "s_begin": a.s_begin, "s_end": a.s_end,
+                        "ops": raw[a.ops_offset:a.ops_offset + a.n_ops].decode()})
+        return res
 
     def search_async(self, query, matrix, alpha: int, beta: int, k: int, d_scores=None, d_topk_ids=None,
                      d_topk_scores=None, stream=None):

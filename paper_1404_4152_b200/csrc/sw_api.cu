@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -30,6 +31,7 @@
 
 #include "../../include/swsearch.h"
 #include "sw_kernels.cuh"
+#include "sw_align.cuh"
 
 using swk::GroupDesc;
 
@@ -120,6 +122,7 @@ struct sw_db {
   int* d_perm = nullptr;          // sorted position -> input index
   int* d_len_sorted = nullptr;    // sorted position -> length
   long long* d_gid = nullptr;     // input index -> global id (nullptr: identity)
+  int* d_inv = nullptr;           // input index -> sorted position (built on the first sw_align)
 
   uint2* d_scratch = nullptr;     // DP boundary rows, one slab per resident warp (inter-task kernels)
   uint2* d_scratch_intra = nullptr; // pass boundaries of the intra-task kernel (runs concurrently: own slabs)
@@ -213,7 +216,7 @@ static void free_db(sw_db* db) {
                   db->d_block_counts, db->d_cnt, db->d_mini_sizes, db->d_mgroups, db->d_mwords, db->d_prof8b,
                   db->d_prof_b, db->d_prof2, db->d_score_sorted2, db->d_flag_b, db->d_scratch_intra,
                   db->d_counters, db->d_hist, db->d_sel,
-                  db->d_topk_ids, db->d_topk_scores, db->d_cub};
+                  db->d_topk_ids, db->d_topk_scores, db->d_cub, db->d_inv};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (db->h_stage) cudaFreeHost(db->h_stage);
@@ -1267,6 +1270,135 @@ int sw_search_batch(sw_db* db, const uint8_t* queries, const int64_t* qoffsets, 
     stats->gcups = stats->seconds > 0 ? (double)stats->cells / stats->seconds / 1e9 : 0.0;
     stats->first_stage = 16;
     stats->reserved[0] = (int32_t)n_pairs;   // query pairs aligned in one pass
+  }
+  return SW_OK;
+}
+
+// ---- f3: traceback of optimal alignments for chosen subjects ----
+constexpr int kAlignTR = 8;                        // query rows per lane of the traceback wavefront
+constexpr int64_t kAlignWorkspace = 1LL << 30;     // direction bytes aligned at once (soft cap)
+
+int sw_align(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix, int32_t alpha, int32_t beta,
+             const int64_t* subjects, int32_t n, sw_alignment* out, char* ops, int64_t ops_cap) {
+  int smax = 0, smin = 0;
+  int rc = validate_search(db, query, qlen, matrix, alpha, beta, 1, &smax, &smin);
+  if (rc) return rc;
+  if (n < 0) return fail(SW_EINVAL, "sw_align: n must be >= 0 (got %d)", n);
+  if (n == 0) return SW_OK;
+  if (!subjects || !out || !ops) return fail(SW_EINVAL, "sw_align: subjects/out/ops must be non-NULL");
+  for (int32_t t = 0; t < n; t++)
+    if (subjects[t] < 0 || subjects[t] >= db->n_seqs)
+      return fail(SW_EINVAL, "sw_align: subjects[%d] = %lld outside [0, %lld)", t, (long long)subjects[t],
+                  (long long)db->n_seqs);
+  std::lock_guard<std::mutex> lock(db->mu);
+  CK(cudaSetDevice(db->device));
+  cudaStream_t st = db->stream;
+  CK(cudaStreamWaitEvent(st, db->ev_done, 0));
+  const int nseq = (int)db->n_seqs;
+  if (!db->d_inv) {
+    CK(cudaMalloc(&db->d_inv, (size_t)nseq * sizeof(int)));
+    swk::k_inverse_perm<<<std::min((nseq + 255) / 256, db->num_sms * 8), 256, 0, st>>>(db->d_perm, nseq, db->d_inv);
+    CK(cudaGetLastError());
+    db->launches++;
+  }
+  // ---- locate the subjects in the packed layout; their lengths size everything ----
+  const int m_pad = (qlen + 7) / 8 * 8;
+  const int stride = (m_pad + 31) / 32 * 32 + 8;
+  const size_t prof_bytes = ((size_t)swk::kProfRows * stride + 15) / 16 * 16;
+  long long* d_idx = nullptr;
+  swk::AlignJob* d_jobs = nullptr;
+  uint8_t* d_q = nullptr;
+  int8_t *d_M = nullptr, *d_prof = nullptr;
+  int* d_res = nullptr;
+  uint32_t* d_dir = nullptr;
+  int2* d_bnd = nullptr;
+  char *d_ops = nullptr, *d_tmp = nullptr;
+  auto release = [&]() {
+    void* ptrs[] = {d_idx, d_jobs, d_q, d_M, d_prof, d_res, d_dir, d_bnd, d_ops, d_tmp};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  };
+  struct Guard { std::function<void()> f; ~Guard() { f(); } } guard{release};
+  CK(cudaMalloc(&d_idx, (size_t)n * sizeof(long long)));
+  CK(cudaMalloc(&d_jobs, (size_t)n * sizeof(swk::AlignJob)));
+  CK(cudaMalloc(&d_res, (size_t)n * 6 * sizeof(int)));
+  CK(cudaMalloc(&d_q, (size_t)qlen));
+  CK(cudaMalloc(&d_M, 1024));
+  CK(cudaMalloc(&d_prof, prof_bytes));
+  CK(cudaMemcpyAsync(d_idx, subjects, (size_t)n * sizeof(long long), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_q, query, (size_t)qlen, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_M, matrix, 1024, cudaMemcpyHostToDevice, st));
+  swk::k_profile<<<64, 256, 0, st>>>(d_q, qlen, d_M, d_prof, stride);
+  swk::k_align_locate<<<(n + 127) / 128, 128, 0, st>>>(d_idx, n, db->d_inv, db->d_len_sorted, db->d_groups, d_jobs);
+  CK(cudaGetLastError());
+  db->launches += 2;
+  std::vector<swk::AlignJob> jobs(n);
+  CK(cudaMemcpyAsync(jobs.data(), d_jobs, (size_t)n * sizeof(swk::AlignJob), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int64_t need = 0;
+  for (int32_t t = 0; t < n; t++) need += (int64_t)qlen + jobs[t].n;
+  if (ops_cap < need)
+    return fail(SW_EINVAL, "sw_align: ops_cap %lld too small, need %lld bytes", (long long)ops_cap, (long long)need);
+  CK(cudaMalloc(&d_ops, (size_t)std::max<int64_t>(need, 1)));
+  CK(cudaMalloc(&d_tmp, (size_t)std::max<int64_t>(need, 1)));
+  // ---- batches of jobs whose direction matrices fit the workspace ----
+  const int64_t rows_blocks = m_pad / kAlignTR;
+  int64_t ops_off = 0, dir_cap = 0, bnd_cap = 0;
+  for (int32_t t = 0; t < n; t++) {
+    jobs[t].ops = ops_off;
+    jobs[t].tmp = ops_off;
+    ops_off += (int64_t)qlen + jobs[t].n;
+  }
+  int64_t ws = kAlignWorkspace;
+  if (const char* e = getenv("SW_ALIGN_WORKSPACE")) ws = std::max<int64_t>(4, atoll(e));   // tests: force batching
+  for (int32_t t0 = 0; t0 < n;) {
+    int32_t t1 = t0;
+    int64_t dsz = 0, bsz = 0;
+    while (t1 < n) {
+      const int64_t d = rows_blocks * jobs[t1].n, b = 2 * (int64_t)jobs[t1].n;
+      if (t1 > t0 && (dsz + d) * 4 > ws) break;
+      jobs[t1].dir = dsz;
+      jobs[t1].bnd = bsz;
+      dsz += d;
+      bsz += b;
+      t1++;
+    }
+    if (dsz > dir_cap) {
+      if (d_dir) cudaFree(d_dir);
+      d_dir = nullptr;
+      CK(cudaMalloc(&d_dir, (size_t)std::max<int64_t>(dsz, 1) * sizeof(uint32_t)));
+      dir_cap = dsz;
+    }
+    if (bsz > bnd_cap) {
+      if (d_bnd) cudaFree(d_bnd);
+      d_bnd = nullptr;
+      CK(cudaMalloc(&d_bnd, (size_t)std::max<int64_t>(bsz, 1) * sizeof(int2)));
+      bnd_cap = bsz;
+    }
+    CK(cudaMemcpyAsync(d_jobs + t0, jobs.data() + t0, (size_t)(t1 - t0) * sizeof(swk::AlignJob),
+                       cudaMemcpyHostToDevice, st));
+    swk::k_align<kAlignTR><<<t1 - t0, 32, 0, st>>>(db->d_words, d_jobs + t0, t1 - t0, d_prof, stride, qlen, m_pad,
+                                                   alpha, beta, d_dir, d_bnd, d_ops, d_tmp, d_res + 6 * t0);
+    CK(cudaGetLastError());
+    db->launches++;
+    CK(cudaStreamSynchronize(st));   // the workspace is reused by the next batch
+    t0 = t1;
+  }
+  std::vector<int> res((size_t)n * 6);
+  CK(cudaMemcpyAsync(res.data(), d_res, res.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ops, d_ops, (size_t)need, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int32_t t = 0; t < n; t++) {
+    sw_alignment& a = out[t];
+    a.subject = subjects[t];
+    a.score = res[6 * t];
+    a.q_begin = res[6 * t + 1];
+    a.q_end = res[6 * t + 2];
+    a.s_begin = res[6 * t + 3];
+    a.s_end = res[6 * t + 4];
+    a.n_ops = res[6 * t + 5];
+    a.reserved = 0;
+    a.ops_offset = jobs[t].ops;
   }
   return SW_OK;
 }
