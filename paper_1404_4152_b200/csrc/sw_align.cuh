@@ -57,7 +57,7 @@ __device__ __forceinline__ bool better(int h, int j, int i, int bh, int bj, int 
 template <int TR>
 __global__ void __launch_bounds__(32)
 k_align(const uint2* __restrict__ words, const AlignJob* __restrict__ jobs, int n_jobs,
-        const int8_t* __restrict__ prof, int stride, int m, int m_pad, int alpha, int beta,
+        const int8_t* __restrict__ prof, int prof_smem, int stride, int m, int m_pad, int alpha, int beta,
         uint32_t* __restrict__ dir, int2* __restrict__ bnd, char* __restrict__ ops_out,
         char* __restrict__ ops_tmp, int* __restrict__ res) {
   const int t = blockIdx.x;
@@ -69,6 +69,16 @@ k_align(const uint2* __restrict__ words, const AlignJob* __restrict__ jobs, int 
   uint32_t* D = dir + J.dir;
   int2* B = bnd + J.bnd;
   int best = 0, bj = 0x7fffffff, bi = 0x7fffffff;
+  // the int8 query profile is staged in shared memory (prof_smem bytes, 0 = read through L1)
+  extern __shared__ __align__(16) int8_t s_prof[];
+  const int8_t* P = prof;
+  if (prof_smem) {
+    const uint4* src = reinterpret_cast<const uint4*>(prof);
+    uint4* dst = reinterpret_cast<uint4*>(s_prof);
+    for (int k = lane; k < prof_smem / 16; k += 32) dst[k] = __ldg(src + k);
+    __syncwarp();
+    P = s_prof;
+  }
   int pass = 0;
   for (int base = 0; n > 0 && base < m_pad; base += 32 * TR, pass++) {
     const int nact = min(32, (m_pad - base) / TR);
@@ -76,50 +86,75 @@ k_align(const uint2* __restrict__ words, const AlignJob* __restrict__ jobs, int 
     const int2* gin = B + (long long)(pass & 1) * n;            // written by the previous pass
     int2* gout = B + (long long)((pass + 1) & 1) * n;
     const int i0 = base + lane * TR;
-    const int8_t* pr = prof + i0;
+    const int8_t* pr = P + i0;
     int Hc[TR], Fc[TR];                                          // H(i, j-1), F(i, j-1)
 #pragma unroll
     for (int r = 0; r < TR; r++) { Hc[r] = 0; Fc[r] = 0; }        // H(i,0) = F(i,0) = 0
     int h_out = 0, e_out = 0, hdiag = 0;                         // hdiag = H(i0-1, j-1)
-    for (int s = 0; s < n + nact - 1; s++) {
-      int h_in = __shfl_up_sync(0xffffffffu, h_out, 1);
-      int e_in = __shfl_up_sync(0xffffffffu, e_out, 1);
-      const int j = s - lane;
-      if (lane == 0) {                                           // row base-1 of column j
-        const int2 g = (!first && j < n) ? gin[j] : make_int2(0, 0);
-        h_in = g.x;
-        e_in = g.y;
-      }
-      if (lane < nact && j >= 0 && j < n) {
-        const uint32_t c = (__ldg(wp + 64 * (j / 6)) >> (5 * (j % 6))) & 31u;
-        const uint2 pv = *reinterpret_cast<const uint2*>(pr + c * stride);
-        int hu = h_in, eu = e_in, dg = hdiag;
-        uint32_t nib = 0;
-#pragma unroll
-        for (int r = 0; r < TR; r++) {
-          const int sub = (int)(int8_t)(((r < 4 ? pv.x : pv.y) >> (8 * (r & 3))) & 0xffu);
-          const int G = dg + sub;                                  // H(i-1,j-1) + fsbt(q_i, s_j)
-          const int eo = hu - beta, ee = eu - alpha;
-          const int E = max(ee, eo);                               // E(i,j)
-          const int fo = Hc[r] - beta, fe = Fc[r] - alpha;
-          const int F = max(fe, fo);                               // F(i,j)
-          const int H = max(max(0, G), max(E, F));
-          const uint32_t src = H == 0 ? 0u : H == G ? 1u : H == E ? 2u : 3u;
-          nib |= (src | (ee > eo ? 4u : 0u) | (fe > fo ? 8u : 0u)) << (4 * r);
-          const int i = i0 + r;
-          if (i < m && better(H, j, i, best, bj, bi)) { best = H; bj = j; bi = i; }
-          dg = Hc[r];                                              // H(i, j-1): diagonal of row i+1
-          Hc[r] = H;
-          Fc[r] = F;
-          hu = H;
-          eu = E;
+    uint32_t c_out = 0;                                          // residue of the column this lane just did
+    // lane 0's per-step inputs (residue of column s, boundary row of column s)
+    // are fetched 32 steps at a time, one block ahead, and handed over by SHFL
+    auto fetch = [&](int sb, uint32_t& rc, int2& gv) {
+      const int c = sb + lane;
+      rc = c < n ? (__ldg(wp + 64 * (c / 6)) >> (5 * (c % 6))) & 31u : 0u;
+      gv = (!first && c < n) ? gin[c] : make_int2(0, 0);
+    };
+    uint32_t rc_cur, rc_nxt;
+    int2 gv_cur, gv_nxt;
+    fetch(0, rc_cur, gv_cur);
+    fetch(32, rc_nxt, gv_nxt);
+    const int nsteps = n + nact - 1;
+    for (int sb = 0; sb < nsteps; sb += 32) {
+#pragma unroll 1
+      for (int tt = 0; tt < 32; tt++) {
+        const int s = sb + tt;
+        if (s >= nsteps) break;
+        int h_in = __shfl_up_sync(0xffffffffu, h_out, 1);
+        int e_in = __shfl_up_sync(0xffffffffu, e_out, 1);
+        uint32_t c = __shfl_up_sync(0xffffffffu, c_out, 1);
+        const uint32_t c0 = __shfl_sync(0xffffffffu, rc_cur, tt);
+        const int g0x = __shfl_sync(0xffffffffu, gv_cur.x, tt);
+        const int g0y = __shfl_sync(0xffffffffu, gv_cur.y, tt);
+        const int j = s - lane;
+        if (lane == 0) {                                         // row base-1 of column j, residue s_j
+          h_in = g0x;
+          e_in = g0y;
+          c = c0;
         }
-        D[(long long)(i0 / TR) * n + j] = nib;
-        if (!last && lane == nact - 1) gout[j] = make_int2(hu, eu);
-        h_out = hu;
-        e_out = eu;
-        hdiag = h_in;                                              // H(i0-1, j) is the next column's diagonal
+        if (lane < nact && j >= 0 && j < n) {
+          const uint2 pv = *reinterpret_cast<const uint2*>(pr + c * stride);
+          int hu = h_in, eu = e_in, dg = hdiag;
+          uint32_t nib = 0;
+#pragma unroll
+          for (int r = 0; r < TR; r++) {
+            const int sub = (int)(int8_t)(((r < 4 ? pv.x : pv.y) >> (8 * (r & 3))) & 0xffu);
+            const int G = dg + sub;                                // H(i-1,j-1) + fsbt(q_i, s_j)
+            const int eo = hu - beta, ee = eu - alpha;
+            const int E = max(ee, eo);                             // E(i,j)
+            const int fo = Hc[r] - beta, fe = Fc[r] - alpha;
+            const int F = max(fe, fo);                             // F(i,j)
+            const int H = max(max(0, G), max(E, F));
+            const uint32_t src = H == 0 ? 0u : H == G ? 1u : H == E ? 2u : 3u;
+            nib |= (src | (ee > eo ? 4u : 0u) | (fe > fo ? 8u : 0u)) << (4 * r);
+            const int i = i0 + r;
+            if (i < m && better(H, j, i, best, bj, bi)) { best = H; bj = j; bi = i; }
+            dg = Hc[r];                                            // H(i, j-1): diagonal of row i+1
+            Hc[r] = H;
+            Fc[r] = F;
+            hu = H;
+            eu = E;
+          }
+          D[(long long)(i0 / TR) * n + j] = nib;
+          if (!last && lane == nact - 1) gout[j] = make_int2(hu, eu);
+          h_out = hu;
+          e_out = eu;
+          c_out = c;
+          hdiag = h_in;                                            // H(i0-1, j) is the next column's diagonal
+        }
       }
+      rc_cur = rc_nxt;
+      gv_cur = gv_nxt;
+      fetch(sb + 64, rc_nxt, gv_nxt);
     }
     __syncwarp();
   }

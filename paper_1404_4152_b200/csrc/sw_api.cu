@@ -123,6 +123,8 @@ struct sw_db {
   int* d_len_sorted = nullptr;    // sorted position -> length
   long long* d_gid = nullptr;     // input index -> global id (nullptr: identity)
   int* d_inv = nullptr;           // input index -> sorted position (built on the first sw_align)
+  void* aw[10] = {};              // sw_align workspace (grow-only): idx, jobs, res, q, M, prof, dir, bnd, ops, tmp
+  size_t aw_cap[10] = {};
 
   uint2* d_scratch = nullptr;     // DP boundary rows, one slab per resident warp (inter-task kernels)
   uint2* d_scratch_intra = nullptr; // pass boundaries of the intra-task kernel (runs concurrently: own slabs)
@@ -218,6 +220,8 @@ static void free_db(sw_db* db) {
                   db->d_counters, db->d_hist, db->d_sel,
                   db->d_topk_ids, db->d_topk_scores, db->d_cub, db->d_inv};
   for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (void* p : db->aw)
     if (p) cudaFree(p);
   if (db->h_stage) cudaFreeHost(db->h_stage);
   if (db->ev_stage) cudaEventDestroy(db->ev_stage);
@@ -1305,26 +1309,16 @@ int sw_align(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix
   const int m_pad = (qlen + 7) / 8 * 8;
   const int stride = (m_pad + 31) / 32 * 32 + 8;
   const size_t prof_bytes = ((size_t)swk::kProfRows * stride + 15) / 16 * 16;
-  long long* d_idx = nullptr;
-  swk::AlignJob* d_jobs = nullptr;
-  uint8_t* d_q = nullptr;
-  int8_t *d_M = nullptr, *d_prof = nullptr;
-  int* d_res = nullptr;
-  uint32_t* d_dir = nullptr;
-  int2* d_bnd = nullptr;
-  char *d_ops = nullptr, *d_tmp = nullptr;
-  auto release = [&]() {
-    void* ptrs[] = {d_idx, d_jobs, d_q, d_M, d_prof, d_res, d_dir, d_bnd, d_ops, d_tmp};
-    for (void* p : ptrs)
-      if (p) cudaFree(p);
+  auto ws = [&](int k, size_t bytes) -> void* {
+    return ensure(&db->aw[k], &db->aw_cap[k], std::max<size_t>(bytes, 16)) == SW_OK ? db->aw[k] : nullptr;
   };
-  struct Guard { std::function<void()> f; ~Guard() { f(); } } guard{release};
-  CK(cudaMalloc(&d_idx, (size_t)n * sizeof(long long)));
-  CK(cudaMalloc(&d_jobs, (size_t)n * sizeof(swk::AlignJob)));
-  CK(cudaMalloc(&d_res, (size_t)n * 6 * sizeof(int)));
-  CK(cudaMalloc(&d_q, (size_t)qlen));
-  CK(cudaMalloc(&d_M, 1024));
-  CK(cudaMalloc(&d_prof, prof_bytes));
+  long long* d_idx = (long long*)ws(0, (size_t)n * sizeof(long long));
+  swk::AlignJob* d_jobs = (swk::AlignJob*)ws(1, (size_t)n * sizeof(swk::AlignJob));
+  int* d_res = (int*)ws(2, (size_t)n * 6 * sizeof(int));
+  uint8_t* d_q = (uint8_t*)ws(3, (size_t)qlen);
+  int8_t* d_M = (int8_t*)ws(4, 1024);
+  int8_t* d_prof = (int8_t*)ws(5, prof_bytes);
+  if (!d_idx || !d_jobs || !d_res || !d_q || !d_M || !d_prof) return SW_ENOMEM;
   CK(cudaMemcpyAsync(d_idx, subjects, (size_t)n * sizeof(long long), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_q, query, (size_t)qlen, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_M, matrix, 1024, cudaMemcpyHostToDevice, st));
@@ -1339,46 +1333,42 @@ int sw_align(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix
   for (int32_t t = 0; t < n; t++) need += (int64_t)qlen + jobs[t].n;
   if (ops_cap < need)
     return fail(SW_EINVAL, "sw_align: ops_cap %lld too small, need %lld bytes", (long long)ops_cap, (long long)need);
-  CK(cudaMalloc(&d_ops, (size_t)std::max<int64_t>(need, 1)));
-  CK(cudaMalloc(&d_tmp, (size_t)std::max<int64_t>(need, 1)));
+  char* d_ops = (char*)ws(8, (size_t)need);
+  char* d_tmp = (char*)ws(9, (size_t)need);
+  if (!d_ops || !d_tmp) return SW_ENOMEM;
   // ---- batches of jobs whose direction matrices fit the workspace ----
   const int64_t rows_blocks = m_pad / kAlignTR;
-  int64_t ops_off = 0, dir_cap = 0, bnd_cap = 0;
+  int64_t ops_off = 0;
   for (int32_t t = 0; t < n; t++) {
     jobs[t].ops = ops_off;
     jobs[t].tmp = ops_off;
     ops_off += (int64_t)qlen + jobs[t].n;
   }
-  int64_t ws = kAlignWorkspace;
-  if (const char* e = getenv("SW_ALIGN_WORKSPACE")) ws = std::max<int64_t>(4, atoll(e));   // tests: force batching
+  const size_t prof_smem = prof_bytes <= (size_t)kMaxSmemProfile ? prof_bytes : 0;
+  CK(cudaFuncSetAttribute(swk::k_align<kAlignTR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)std::max<size_t>(prof_smem, 1)));
+  int64_t ws_cap = kAlignWorkspace;
+  if (const char* e = getenv("SW_ALIGN_WORKSPACE")) ws_cap = std::max<int64_t>(4, atoll(e));   // tests: force batching
   for (int32_t t0 = 0; t0 < n;) {
     int32_t t1 = t0;
     int64_t dsz = 0, bsz = 0;
     while (t1 < n) {
       const int64_t d = rows_blocks * jobs[t1].n, b = 2 * (int64_t)jobs[t1].n;
-      if (t1 > t0 && (dsz + d) * 4 > ws) break;
+      if (t1 > t0 && (dsz + d) * 4 > ws_cap) break;
       jobs[t1].dir = dsz;
       jobs[t1].bnd = bsz;
       dsz += d;
       bsz += b;
       t1++;
     }
-    if (dsz > dir_cap) {
-      if (d_dir) cudaFree(d_dir);
-      d_dir = nullptr;
-      CK(cudaMalloc(&d_dir, (size_t)std::max<int64_t>(dsz, 1) * sizeof(uint32_t)));
-      dir_cap = dsz;
-    }
-    if (bsz > bnd_cap) {
-      if (d_bnd) cudaFree(d_bnd);
-      d_bnd = nullptr;
-      CK(cudaMalloc(&d_bnd, (size_t)std::max<int64_t>(bsz, 1) * sizeof(int2)));
-      bnd_cap = bsz;
-    }
+    uint32_t* d_dir = (uint32_t*)ws(6, (size_t)dsz * sizeof(uint32_t));
+    int2* d_bnd = (int2*)ws(7, (size_t)bsz * sizeof(int2));
+    if (!d_dir || !d_bnd) return SW_ENOMEM;
     CK(cudaMemcpyAsync(d_jobs + t0, jobs.data() + t0, (size_t)(t1 - t0) * sizeof(swk::AlignJob),
                        cudaMemcpyHostToDevice, st));
-    swk::k_align<kAlignTR><<<t1 - t0, 32, 0, st>>>(db->d_words, d_jobs + t0, t1 - t0, d_prof, stride, qlen, m_pad,
-                                                   alpha, beta, d_dir, d_bnd, d_ops, d_tmp, d_res + 6 * t0);
+    swk::k_align<kAlignTR><<<t1 - t0, 32, prof_smem, st>>>(db->d_words, d_jobs + t0, t1 - t0, d_prof, (int)prof_smem,
+                                                           stride, qlen, m_pad, alpha, beta, d_dir, d_bnd, d_ops,
+                                                           d_tmp, d_res + 6 * t0);
     CK(cudaGetLastError());
     db->launches++;
     CK(cudaStreamSynchronize(st));   // the workspace is reused by the next batch
