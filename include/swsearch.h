@@ -69,7 +69,13 @@ typedef struct sw_opts {
   int32_t long_threshold; /* subjects longer than this use the intra-task wavefront kernel;
                              0 = library default, -1 = never (all inter-task) */
   int32_t verbose;        /* 0 = silent */
-  int32_t reserved[4];    /* must be 0 */
+  int32_t residency;      /* 0 = packed database resident in device memory (default);
+                             1 = kept in pinned host memory and streamed to the device
+                             in chunks during every search (f2: databases larger than
+                             HBM; first_stage 16 or 32; not with sw_search_batch) */
+  int32_t chunk_mb;       /* residency 1: device bytes per streamed chunk in MiB
+                             (two are allocated); 0 = 512 */
+  int32_t reserved[2];    /* must be 0 */
 } sw_opts;
 
 typedef struct sw_stats {
@@ -97,10 +103,12 @@ typedef struct sw_db_info {
   int32_t max_len;              /* longest subject */
   int32_t device;
   int32_t long_threshold;
-  int32_t reserved[5];
+  int32_t residency;            /* as sw_opts.residency */
+  int32_t n_chunks;             /* residency 1: chunks streamed per search */
+  int32_t reserved[3];
 } sw_db_info;
 
-/* Fill *opts with defaults (device -1, first_stage 16, long_threshold 0). */
+/* Fill *opts with defaults (device -1, first_stage 16, long_threshold 0, residency 0). */
 void sw_opts_default(sw_opts* opts);
 
 /*

@@ -32,7 +32,8 @@ class SwError(RuntimeError):
 class sw_opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("first_stage", ctypes.c_int32),
                 ("long_threshold", ctypes.c_int32), ("verbose", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("residency", ctypes.c_int32), ("chunk_mb", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class sw_stats(ctypes.Structure):
@@ -52,7 +53,8 @@ class sw_db_info(ctypes.Structure):
                 ("n_intra", ctypes.c_int64), ("n_groups", ctypes.c_int64), ("packed_bytes", ctypes.c_int64),
                 ("scratch_bytes", ctypes.c_int64), ("launches", ctypes.c_int64), ("n_searches", ctypes.c_int64),
                 ("max_len", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("long_threshold", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("long_threshold", ctypes.c_int32), ("residency", ctypes.c_int32), ("n_chunks", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 class sw_alignment(ctypes.Structure):
@@ -135,7 +137,7 @@ class Database:
     """sw_db_create / sw_db_destroy.  Arrays are copied (and packed) by the library."""
 
     def __init__(self, residues, offsets, lengths, global_ids=None, device: int = -1,
-                 first_stage: int = 16, long_threshold: int = 0):
+                 first_stage: int = 16, long_threshold: int = 0, residency: int = 0, chunk_mb: int = 0):
         L = lib()
         res = np.ascontiguousarray(residues, dtype=np.uint8)
         offs = np.ascontiguousarray(offsets, dtype=np.int64)
@@ -146,6 +148,7 @@ class Database:
         o = sw_opts()
         L.sw_opts_default(ctypes.byref(o))
         o.device, o.first_stage, o.long_threshold = device, first_stage, long_threshold
+        o.residency, o.chunk_mb = residency, chunk_mb
         h = ctypes.c_void_p()
         _check(L.sw_db_create(_ptr(res) if res.size else None, res.size, _ptr(offs) if offs.size else None,
                               _ptr(lens) if lens.size else None, lens.size,
@@ -159,12 +162,14 @@ class Database:
         return cls(db.residues, db.offsets, db.lengths, **kw)
 
     @classmethod
-    def load(cls, path: str, device: int = -1, first_stage: int = 16, long_threshold: int = 0) -> "Database":
+    def load(cls, path: str, device: int = -1, first_stage: int = 16, long_threshold: int = 0,
+             residency: int = 0, chunk_mb: int = 0) -> "Database":
         """sw_db_load: map a file written by save() and upload it (no re-sort / re-pack)."""
         L = lib()
         o = sw_opts()
         L.sw_opts_default(ctypes.byref(o))
         o.device, o.first_stage, o.long_threshold = device, first_stage, long_threshold
+        o.residency, o.chunk_mb = residency, chunk_mb
         h = ctypes.c_void_p()
         _check(L.sw_db_load(os.fsencode(path), ctypes.byref(o), ctypes.byref(h)))
         self = cls.__new__(cls)

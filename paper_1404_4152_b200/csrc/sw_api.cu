@@ -117,6 +117,17 @@ struct sw_db {
   int64_t n_groups = 0, n_words = 0;
   std::vector<int> group_ncols;   // host copy (ascending): picks the intra-task groups per search
 
+  // f2 host residency: packed words in pinned (mapped) host memory, streamed per search
+  bool host_resident = false;
+  uint2* h_words = nullptr;
+  std::vector<int64_t> h_group_base;                 // n_groups + 1 word offsets
+  std::vector<std::pair<int64_t, int64_t>> chunks;   // [g0, g1) per streamed chunk
+  int64_t chunk_words = 0;
+  uint2* d_chunk[2] = {nullptr, nullptr};
+  int* d_stream_cnt = nullptr;                       // int32 reruns per chunk
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+
   uint2* d_words = nullptr;
   GroupDesc* d_groups = nullptr;
   int* d_perm = nullptr;          // sorted position -> input index
@@ -218,11 +229,18 @@ static void free_db(sw_db* db) {
                   db->d_block_counts, db->d_cnt, db->d_mini_sizes, db->d_mgroups, db->d_mwords, db->d_prof8b,
                   db->d_prof_b, db->d_prof2, db->d_score_sorted2, db->d_flag_b, db->d_scratch_intra,
                   db->d_counters, db->d_hist, db->d_sel,
-                  db->d_topk_ids, db->d_topk_scores, db->d_cub, db->d_inv};
+                  db->d_topk_ids, db->d_topk_scores, db->d_cub, db->d_inv, db->d_chunk[0], db->d_chunk[1],
+                  db->d_stream_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (void* p : db->aw)
     if (p) cudaFree(p);
+  if (db->h_words) cudaFreeHost(db->h_words);
+  for (int b = 0; b < 2; b++) {
+    if (db->ev_copied[b]) cudaEventDestroy(db->ev_copied[b]);
+    if (db->ev_consumed[b]) cudaEventDestroy(db->ev_consumed[b]);
+  }
+  if (db->copy_stream) cudaStreamDestroy(db->copy_stream);
   if (db->h_stage) cudaFreeHost(db->h_stage);
   if (db->ev_stage) cudaEventDestroy(db->ev_stage);
   if (db->ev_done) cudaEventDestroy(db->ev_done);
@@ -249,6 +267,8 @@ int sw_db_get_info(const sw_db* db, sw_db_info* info) {
   info->max_len = db->max_len;
   info->device = db->device;
   info->long_threshold = db->long_threshold;
+  info->residency = db->host_resident ? 1 : 0;
+  info->n_chunks = (int32_t)db->chunks.size();
   info->launches = db->launches;
   info->n_searches = db->n_searches;
   return SW_OK;
@@ -296,6 +316,19 @@ static int validate_db(const uint8_t* residues, int64_t n_residues, const int64_
 }
 
 static int finish_create(sw_db* db);
+
+static int validate_residency(const sw_opts& o) {
+  if (o.residency != 0 && o.residency != 1) return fail(SW_EINVAL, "residency must be 0 or 1 (got %d)", o.residency);
+  if (o.residency == 1 && o.first_stage == 8)
+    return fail(SW_EINVAL, "residency 1 (streamed) supports first_stage 16 or 32, not 8");
+  if (o.chunk_mb < 0 || o.chunk_mb > (1 << 20)) return fail(SW_EINVAL, "chunk_mb out of range (got %d)", o.chunk_mb);
+  return SW_OK;
+}
+
+static void set_residency(sw_db* db, const sw_opts& o) {
+  db->host_resident = o.residency == 1;
+  db->chunk_words = (int64_t)(o.chunk_mb > 0 ? o.chunk_mb : 512) * (1 << 20) / (int64_t)sizeof(uint2);
+}
 
 static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_t* offsets,
                        const int32_t* lengths, int64_t n_seqs, const int64_t* gids, const sw_opts* o,
@@ -346,14 +379,23 @@ static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_
   db->group_ncols.resize(n_groups);
   for (int64_t g = 0; g < n_groups; g++) db->group_ncols[g] = groups[g].ncols;
 
-  CK(cudaMalloc(&db->d_words, std::max<int64_t>(base, 1) * sizeof(uint2)));
+  db->h_group_base.resize(n_groups + 1);
+  for (int64_t g = 0; g < n_groups; g++) db->h_group_base[g] = groups[g].base;
+  db->h_group_base[n_groups] = base;
+  if (db->host_resident)
+    CK(cudaHostAlloc(&db->h_words, std::max<int64_t>(base, 1) * sizeof(uint2), cudaHostAllocMapped | cudaHostAllocPortable));
+  else
+    CK(cudaMalloc(&db->d_words, std::max<int64_t>(base, 1) * sizeof(uint2)));
   {
     // pack group ranges into two pinned staging buffers, upload overlapped
+    // (host residency: pack straight into the pinned host copy, no upload)
     const int64_t kChunkWords = 1 << 24;   // 128 MB of uint2
     uint2* stage[2] = {nullptr, nullptr};
     cudaEvent_t ev[2];
-    CK(cudaHostAlloc(&stage[0], kChunkWords * sizeof(uint2), cudaHostAllocDefault));
-    CK(cudaHostAlloc(&stage[1], kChunkWords * sizeof(uint2), cudaHostAllocDefault));
+    if (!db->host_resident) {
+      CK(cudaHostAlloc(&stage[0], kChunkWords * sizeof(uint2), cudaHostAllocDefault));
+      CK(cudaHostAlloc(&stage[1], kChunkWords * sizeof(uint2), cudaHostAllocDefault));
+    }
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     int64_t g0 = 0;
@@ -370,8 +412,8 @@ static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_
       }
       if (rc != SW_OK) break;
       if (used[buf]) cudaEventSynchronize(ev[buf]);
-      uint2* st = stage[buf];
       const int64_t wbase = groups[g0].base;
+      uint2* st = db->host_resident ? db->h_words + wbase : stage[buf];
       const int64_t wend = (g1 < n_groups ? groups[g1].base : base);
       parallel_for(g1 - g0, [&](int64_t a, int64_t b) {
         for (int64_t gg = g0 + a; gg < g0 + b; gg++) {
@@ -399,17 +441,19 @@ static int create_impl(const uint8_t* residues, int64_t n_residues, const int64_
           }
         }
       });
-      cudaError_t e = cudaMemcpyAsync(db->d_words + wbase, st, (wend - wbase) * sizeof(uint2),
-                                      cudaMemcpyHostToDevice, db->stream);
-      if (e != cudaSuccess) { rc = fail(SW_ECUDA, "upload: %s", cudaGetErrorString(e)); break; }
+      if (!db->host_resident) {
+        cudaError_t e = cudaMemcpyAsync(db->d_words + wbase, st, (wend - wbase) * sizeof(uint2),
+                                        cudaMemcpyHostToDevice, db->stream);
+        if (e != cudaSuccess) { rc = fail(SW_ECUDA, "upload: %s", cudaGetErrorString(e)); break; }
+      }
       cudaEventRecord(ev[buf], db->stream);
       used[buf] = true;
       buf ^= 1;
       g0 = g1;
     }
     cudaStreamSynchronize(db->stream);
-    cudaFreeHost(stage[0]);
-    cudaFreeHost(stage[1]);
+    if (stage[0]) cudaFreeHost(stage[0]);
+    if (stage[1]) cudaFreeHost(stage[1]);
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
     if (rc != SW_OK) return rc;
@@ -474,6 +518,30 @@ static int finish_create(sw_db* db) {
   CK(cudaMemset(db->d_hist, 0, 256 * sizeof(unsigned)));
   CK(cudaMalloc(&db->d_sel, sizeof(swk::SelState)));
   CK(cudaMalloc(&db->d_matrix, 32 * 32));
+  if (db->host_resident) {
+    // chunks of whole groups, at most chunk_words each (a group never splits)
+    int64_t maxg = 0;
+    for (int64_t g = 0; g < db->n_groups; g++)
+      maxg = std::max(maxg, db->h_group_base[g + 1] - db->h_group_base[g]);
+    db->chunk_words = std::max(db->chunk_words, std::max<int64_t>(maxg, 1));
+    db->chunks.clear();
+    for (int64_t g0 = 0; g0 < db->n_groups;) {
+      int64_t g1 = g0 + 1;
+      while (g1 < db->n_groups && db->h_group_base[g1 + 1] - db->h_group_base[g0] <= db->chunk_words) g1++;
+      db->chunks.emplace_back(g0, g1);
+      g0 = g1;
+    }
+    const int64_t cw = std::min(db->chunk_words, std::max<int64_t>(db->n_words, 1));
+    CK(cudaMalloc(&db->d_chunk[0], cw * sizeof(uint2)));
+    CK(cudaMalloc(&db->d_chunk[1], cw * sizeof(uint2)));
+    CK(cudaMalloc(&db->d_stream_cnt, std::max<size_t>(db->chunks.size(), 1) * sizeof(int)));
+    CK(cudaMemset(db->d_stream_cnt, 0, std::max<size_t>(db->chunks.size(), 1) * sizeof(int)));
+    CK(cudaStreamCreateWithFlags(&db->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; b++) {
+      CK(cudaEventCreateWithFlags(&db->ev_copied[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&db->ev_consumed[b], cudaEventDisableTiming));
+    }
+  }
   CK(cudaEventCreateWithFlags(&db->ev_stage, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&db->ev_done, cudaEventDisableTiming));
   for (auto& set : db->ev_ring)
@@ -492,6 +560,10 @@ int sw_db_create(const uint8_t* residues, int64_t n_residues, const int64_t* off
   if (o.first_stage != 8 && o.first_stage != 16 && o.first_stage != 32)
     return fail(SW_EINVAL, "first_stage must be 8, 16 or 32 (got %d)", o.first_stage);
   {
+    int rc = validate_residency(o);
+    if (rc != SW_OK) return rc;
+  }
+  {
     int rc = validate_db(residues, n_residues, offsets, lengths, n_seqs, global_ids);
     if (rc != SW_OK) return rc;
   }
@@ -503,6 +575,7 @@ int sw_db_create(const uint8_t* residues, int64_t n_residues, const int64_t* off
     db->device = o.device;
   }
   db->first_stage = o.first_stage;
+  set_residency(db, o);
   cudaError_t e = cudaSetDevice(db->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&db->num_sms, cudaDevAttrMultiProcessorCount, db->device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&db->stream, cudaStreamNonBlocking);
@@ -569,7 +642,7 @@ int sw_db_save(sw_db* db, const char* path) {
     std::vector<char> buf((size_t)std::min<int64_t>(bytes, 1 << 26));
     for (int64_t done = 0; done < bytes && rc == SW_OK; done += (int64_t)buf.size()) {
       const int64_t c = std::min<int64_t>((int64_t)buf.size(), bytes - done);
-      cudaError_t e = cudaMemcpy(buf.data(), (const char*)dev + done, c, cudaMemcpyDeviceToHost);
+      cudaError_t e = cudaMemcpy(buf.data(), (const char*)dev + done, c, cudaMemcpyDefault);
       if (e != cudaSuccess) { rc = fail(SW_ECUDA, "sw_db_save: %s", cudaGetErrorString(e)); return; }
       if (fseeko(f, off + done, SEEK_SET) != 0 || fwrite(buf.data(), 1, c, f) != (size_t)c)
         rc = fail(SW_EINVAL, "sw_db_save: write failed on %s", path);
@@ -580,7 +653,8 @@ int sw_db_save(sw_db* db, const char* path) {
   put(h.off_perm, db->d_perm, h.n_seqs * 4);
   put(h.off_len, db->d_len_sorted, h.n_seqs * 4);
   if (h.has_gid) put(h.off_gid, db->d_gid, h.n_seqs * 8);
-  put(h.off_words, db->d_words, h.n_words * (int64_t)sizeof(uint2));
+  put(h.off_words, db->host_resident ? (const void*)db->h_words : (const void*)db->d_words,
+      h.n_words * (int64_t)sizeof(uint2));
   if (fclose(f) != 0 && rc == SW_OK) rc = fail(SW_EINVAL, "sw_db_save: close failed on %s", path);
   return rc;
 }
@@ -606,7 +680,14 @@ static int load_impl(const char* map, const DbFileHeader& h, sw_db* db) {
     expect_base += (int64_t)(groups[g].ncols + swk::kResPerWord - 1) / swk::kResPerWord * 32;
   }
   if (expect_base != h.n_words) return fail(SW_EINVAL, "sw_db_load: group table / word count mismatch");
-  CK(cudaMalloc(&db->d_words, std::max<int64_t>(h.n_words, 1) * sizeof(uint2)));
+  db->h_group_base.resize(h.n_groups + 1);
+  for (int64_t g = 0; g < h.n_groups; g++) db->h_group_base[g] = groups[g].base;
+  db->h_group_base[h.n_groups] = h.n_words;
+  if (db->host_resident)
+    CK(cudaHostAlloc(&db->h_words, std::max<int64_t>(h.n_words, 1) * sizeof(uint2),
+                     cudaHostAllocMapped | cudaHostAllocPortable));
+  else
+    CK(cudaMalloc(&db->d_words, std::max<int64_t>(h.n_words, 1) * sizeof(uint2)));
   CK(cudaMalloc(&db->d_groups, std::max<int64_t>(h.n_groups, 1) * sizeof(GroupDesc)));
   CK(cudaMalloc(&db->d_perm, std::max<int64_t>(h.n_seqs, 1) * sizeof(int)));
   CK(cudaMalloc(&db->d_len_sorted, std::max<int64_t>(h.n_seqs, 1) * sizeof(int)));
@@ -640,7 +721,17 @@ static int load_impl(const char* map, const DbFileHeader& h, sw_db* db) {
     if (cudaMalloc(&db->d_gid, h.n_seqs * sizeof(long long)) != cudaSuccess) rc = fail(SW_ENOMEM, "sw_db_load: gid");
     up(db->d_gid, map + h.off_gid, h.n_seqs * 8);
   }
-  up(db->d_words, map + h.off_words, h.n_words * (int64_t)sizeof(uint2));
+  if (db->host_resident) {
+    const char* src = map + h.off_words;
+    char* dst = (char*)db->h_words;
+    const int64_t bytes = h.n_words * (int64_t)sizeof(uint2);
+    parallel_for((bytes + (1 << 20) - 1) >> 20, [&](int64_t a, int64_t b) {
+      const int64_t lo = a << 20, hi = std::min<int64_t>(bytes, b << 20);
+      if (hi > lo) memcpy(dst + lo, src + lo, (size_t)(hi - lo));
+    });
+  } else {
+    up(db->d_words, map + h.off_words, h.n_words * (int64_t)sizeof(uint2));
+  }
   cudaStreamSynchronize(db->stream);
   cudaFreeHost(stage[0]);
   cudaFreeHost(stage[1]);
@@ -658,6 +749,10 @@ int sw_db_load(const char* path, const sw_opts* opts, sw_db** out) {
   if (opts) o = *opts;
   if (o.first_stage != 8 && o.first_stage != 16 && o.first_stage != 32)
     return fail(SW_EINVAL, "first_stage must be 8, 16 or 32 (got %d)", o.first_stage);
+  {
+    int rc = validate_residency(o);
+    if (rc != SW_OK) return rc;
+  }
   const int fd = open(path, O_RDONLY);
   if (fd < 0) return fail(SW_EINVAL, "sw_db_load: cannot open %s", path);
   struct stat sb;
@@ -686,6 +781,7 @@ int sw_db_load(const char* path, const sw_opts* opts, sw_db** out) {
   if (!db) return bad("host allocation");
   db->first_stage = o.first_stage;
   db->long_threshold = o.long_threshold;
+  set_residency(db, o);
   cudaError_t e = cudaSuccess;
   if (o.device < 0) e = cudaGetDevice(&db->device);
   else db->device = o.device;
@@ -872,12 +968,12 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   const int n_long = (int)(db->group_ncols.end() -
                            std::upper_bound(db->group_ncols.begin(), db->group_ncols.end(), cut));
   db->last_n_long = n_long;
-  const int nb_scan = std::max(1, (n + swk::kScanBlock - 1) / swk::kScanBlock);
-  // compaction of a flag byte array into an ascending list of sorted positions
-  auto compact = [&](uint8_t* flag, int* list, int* count, int* tail_groups) -> int {
-    swk::k_flag_count<<<nb_scan, swk::kScanBlock, 0, st>>>(flag, n, db->d_block_counts);
+  // compaction of a flag byte array (nr positions) into an ascending list of positions
+  auto compact = [&](uint8_t* flag, int nr, int* list, int* count, int* tail_groups) -> int {
+    const int nb_scan = std::max(1, (nr + swk::kScanBlock - 1) / swk::kScanBlock);
+    swk::k_flag_count<<<nb_scan, swk::kScanBlock, 0, st>>>(flag, nr, db->d_block_counts);
     swk::k_scan_exclusive<<<1, swk::kScanBlock, 0, st>>>(db->d_block_counts, nb_scan, count, tail_groups);
-    swk::k_flag_scatter<<<nb_scan, swk::kScanBlock, 0, st>>>(flag, n, db->d_block_counts, list);
+    swk::k_flag_scatter<<<nb_scan, swk::kScanBlock, 0, st>>>(flag, nr, db->d_block_counts, list);
     nl += 3;
     CK(cudaGetLastError());
     return SW_OK;
@@ -899,15 +995,17 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   // everything after it on the stream sees both.  Both take work longest-first
   // from their own counters.
   auto launch16 = [&](const uint2* words, const GroupDesc* groups, int n_groups_i, const int* n_groups_dev,
-                      const int* pos_map, bool any_long, int* counter_inter, int* counter_intra) -> int {
+                      const int* pos_map, int n_long_r, int* counter_inter, int* counter_intra, int* score_out,
+                      uint8_t* flag_out) -> int {
+    const bool any_long = n_long_r > 0;
     long long scols = db->scratch_cols;
     void* kargs_inter[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &cut,
                            &db->d_prof, (void*)&m_pad, (void*)&stride, &alpha, &beta, (void*)&limit16, &db->d_scratch,
-                           &scols, &counter_inter, &db->d_score_sorted, &db->d_flag16};
+                           &scols, &counter_inter, &score_out, &flag_out};
     long long scols_intra = db->scratch_cols_intra;
     void* kargs_intra[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &cut,
                            &db->d_prof, (void*)&m_pad, (void*)&stride, &alpha, &beta, (void*)&limit16,
-                           &db->d_scratch_intra, &scols_intra, &counter_intra, &db->d_score_sorted, &db->d_flag16};
+                           &db->d_scratch_intra, &scols_intra, &counter_intra, &score_out, &flag_out};
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
@@ -918,7 +1016,7 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
     if (any_long) {
       // only as many CTAs as the pair items need (12 warps each): idle CTAs would
       // hold SMs the inter-task kernel could use
-      const int64_t items = (int64_t)(n_groups_dev ? n_groups_i : n_long) * 32;
+      const int64_t items = (int64_t)(n_groups_dev ? n_groups_i : n_long_r) * 32;
       const int grid_intra = (int)std::max<int64_t>(1, std::min<int64_t>(grid, (items + 11) / 12));
       CK(cudaLaunchKernel(kintra, dim3(grid_intra), dim3(swk::kInterThreads), kargs_intra, smem_bytes, st));
       nl++;
@@ -934,6 +1032,42 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   const int bias = -std::min(0, smin);
   const bool stage8 = db->first_stage == 8 && beta <= 255 && smax + bias <= 255;
   db->last_first_stage = db->first_stage == 32 ? 32 : (stage8 ? 8 : 16);
+  auto k32 = smem ? swk::k_list32<kTileRows, true> : swk::k_list32<kTileRows, false>;
+  CK(cudaFuncSetAttribute(k32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
+  // First pass + escalation over the groups [g0, g1) whose packed words sit at
+  // wb + groups[g].base (the whole resident layout, or one streamed chunk).
+  // Positions, scores and flags of the range start at g0 * 64.
+  auto run_range = [&](const uint2* wb, int64_t g0, int64_t g1, int* cnt32, bool mark_ev2) -> int {
+    const int64_t p0 = g0 * swk::kGroup, p1 = std::min<int64_t>(g1 * swk::kGroup, n);
+    const int nr = (int)(p1 - p0);
+    const GroupDesc* gr = db->d_groups + g0;
+    int* sc = db->d_score_sorted + p0;
+    const int* ls = db->d_len_sorted + p0;
+    CK(cudaMemsetAsync(db->d_counters, 0, 8 * sizeof(int), st));
+    if (db->first_stage != 32) {
+      const int n_long_r = (int)((db->group_ncols.begin() + g1) -
+                                 std::upper_bound(db->group_ncols.begin() + g0, db->group_ncols.begin() + g1, cut));
+      uint8_t* fl = db->d_flag16 + p0;
+      int rc = launch16(wb, gr, (int)(g1 - g0), nullptr, nullptr, n_long_r, db->d_counters + 0, db->d_counters + 6, sc,
+                        fl);
+      if (rc) return rc;
+      if (mark_ev2) CK(cudaEventRecord(ev[2], st));
+      // escalation 16 -> 32: rerun only the subjects flagged by the int16 pass (count read on device)
+      rc = compact(fl, nr, db->d_list16, cnt32, nullptr);
+      if (rc) return rc;
+      k32<<<grid, swk::kInterThreads, smem_bytes, st>>>(wb, gr, db->d_list16, cnt32, 0, ls, db->d_prof, m_pad, stride,
+                                                        alpha, beta, db->d_scratch, db->scratch_cols,
+                                                        db->d_counters + 2, sc);
+    } else {
+      if (mark_ev2) CK(cudaEventRecord(ev[2], st));
+      k32<<<grid, swk::kInterThreads, smem_bytes, st>>>(wb, gr, nullptr, nullptr, nr, ls, db->d_prof, m_pad, stride,
+                                                        alpha, beta, db->d_scratch, db->scratch_cols,
+                                                        db->d_counters + 2, sc);
+    }
+    CK(cudaGetLastError());
+    nl++;
+    return SW_OK;
+  };
   if (db->n_inter > 0) {
     if (db->first_stage != 32) CK(cudaMemsetAsync(db->d_flag16, 0, (size_t)n, st));
     if (stage8) {
@@ -950,7 +1084,7 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
       CK(cudaGetLastError());
       CK(cudaEventRecord(ev[2], st));
       // escalation 8 -> 16: compact, re-interleave the flagged subjects, int16 pass on the mini layout
-      int rc = compact(db->d_flag8, db->d_list8, db->d_cnt + 0, db->d_cnt + 2);
+      int rc = compact(db->d_flag8, n, db->d_list8, db->d_cnt + 0, db->d_cnt + 2);
       if (rc) return rc;
       const int nmm = (int)db->n_mini_max;
       swk::k_mini_sizes<<<std::min((nmm + 255) / 256, 4096), 256, 0, st>>>(db->d_list8, db->d_cnt + 0,
@@ -961,35 +1095,40 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
                                                                       nmm, db->d_mgroups, db->d_mwords);
       nl += 3;
       CK(cudaGetLastError());
-      rc = launch16(db->d_mwords, db->d_mgroups, nmm, db->d_cnt + 2, db->d_list8, true, db->d_counters + 4,
-                    db->d_counters + 7);
+      rc = launch16(db->d_mwords, db->d_mgroups, nmm, db->d_cnt + 2, db->d_list8, nmm, db->d_counters + 4,
+                    db->d_counters + 7, db->d_score_sorted, db->d_flag16);
       if (rc) return rc;
-    } else if (db->first_stage != 32) {
-      int rc = launch16(db->d_words, db->d_groups, (int)db->n_groups, nullptr, nullptr, n_long > 0, db->d_counters + 0,
-                        db->d_counters + 6);
-      if (rc) return rc;
-      CK(cudaEventRecord(ev[2], st));
-    } else {
-      CK(cudaEventRecord(ev[2], st));
-    }
-    auto k32 = smem ? swk::k_list32<kTileRows, true> : swk::k_list32<kTileRows, false>;
-    CK(cudaFuncSetAttribute(k32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
-    if (db->first_stage != 32) {
-      // escalation 16 -> 32: rerun only the subjects flagged by the int16 pass (count read on device)
-      int rc = compact(db->d_flag16, db->d_list16, db->d_cnt + 1, nullptr);
+      rc = compact(db->d_flag16, n, db->d_list16, db->d_cnt + 1, nullptr);
       if (rc) return rc;
       k32<<<grid, swk::kInterThreads, smem_bytes, st>>>(
           db->d_words, db->d_groups, db->d_list16, db->d_cnt + 1, 0, db->d_len_sorted, db->d_prof,
           m_pad, stride, alpha, beta, db->d_scratch, db->scratch_cols, db->d_counters + 2,
           db->d_score_sorted);
+      CK(cudaGetLastError());
+      nl++;
+    } else if (!db->host_resident) {
+      int rc = run_range(db->d_words, 0, db->n_groups, db->d_cnt + 1, true);
+      if (rc) return rc;
     } else {
-      k32<<<grid, swk::kInterThreads, smem_bytes, st>>>(
-          db->d_words, db->d_groups, nullptr, nullptr, (int)db->n_inter, db->d_len_sorted, db->d_prof,
-          m_pad, stride, alpha, beta, db->d_scratch, db->scratch_cols, db->d_counters + 2,
-          db->d_score_sorted);
+      // f2: the packed words stay in pinned host memory; chunks of whole groups are
+      // copied on the copy stream into two device buffers while the previous chunk
+      // is aligned (double buffering; PAPER.md:55's chunk-by-chunk offload)
+      CK(cudaEventRecord(ev[2], st));
+      for (size_t c = 0; c < db->chunks.size(); c++) {
+        const int b = (int)(c & 1);
+        const int64_t g0 = db->chunks[c].first, g1 = db->chunks[c].second;
+        const int64_t w0 = db->h_group_base[g0], w1 = db->h_group_base[g1];
+        CK(cudaStreamWaitEvent(db->copy_stream, db->ev_consumed[b], 0));
+        CK(cudaMemcpyAsync(db->d_chunk[b], db->h_words + w0, (size_t)(w1 - w0) * sizeof(uint2),
+                           cudaMemcpyHostToDevice, db->copy_stream));
+        CK(cudaEventRecord(db->ev_copied[b], db->copy_stream));
+        CK(cudaStreamWaitEvent(st, db->ev_copied[b], 0));
+        const uint2* wb = (const uint2*)((uintptr_t)db->d_chunk[b] - (uintptr_t)(w0 * (int64_t)sizeof(uint2)));
+        int rc = run_range(wb, g0, g1, db->d_stream_cnt + c, false);
+        if (rc) return rc;
+        CK(cudaEventRecord(db->ev_consumed[b], st));
+      }
     }
-    CK(cudaGetLastError());
-    nl++;
   } else {
     CK(cudaEventRecord(ev[2], st));
   }
@@ -1051,7 +1190,14 @@ int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matri
   if (topk_scores) CK(cudaMemcpyAsync(topk_scores, db->d_topk_scores, (size_t)k * sizeof(int), cudaMemcpyDeviceToHost, st));
   int cnt[4] = {0};
   CK(cudaMemcpyAsync(cnt, db->d_cnt, sizeof cnt, cudaMemcpyDeviceToHost, st));
+  std::vector<int> ccnt(db->chunks.size());
+  if (db->host_resident && !ccnt.empty())
+    CK(cudaMemcpyAsync(ccnt.data(), db->d_stream_cnt, ccnt.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (db->host_resident) {
+    cnt[1] = 0;
+    for (int c : ccnt) cnt[1] += c;
+  }
   const auto t1 = std::chrono::steady_clock::now();
   if (stats) {
     memset(stats, 0, sizeof *stats);
@@ -1188,6 +1334,8 @@ int sw_search_batch(sw_db* db, const uint8_t* queries, const int64_t* qoffsets, 
   const auto t0 = std::chrono::steady_clock::now();
   if (!db) return fail(SW_EINVAL, "db is NULL");
   if (n_queries < 1 || !queries || !qoffsets || !qlens) return fail(SW_EINVAL, "need n_queries >= 1 and non-NULL query arrays");
+  if (db->host_resident)
+    return fail(SW_EINVAL, "sw_search_batch needs a device-resident database (residency 0); use sw_search per query");
   int smax = 0, smin = 0;
   for (int q = 0; q < n_queries; q++) {
     if (qoffsets[q] < 0) return fail(SW_EINVAL, "query %d: negative offset", q);
@@ -1344,6 +1492,12 @@ int sw_align(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix
     jobs[t].tmp = ops_off;
     ops_off += (int64_t)qlen + jobs[t].n;
   }
+  const uint2* words_dev = db->d_words;
+  if (db->host_resident) {   // streamed database: read the few hits' words from mapped pinned memory
+    void* p = nullptr;
+    CK(cudaHostGetDevicePointer(&p, db->h_words, 0));
+    words_dev = (const uint2*)p;
+  }
   const size_t prof_smem = prof_bytes <= (size_t)kMaxSmemProfile ? prof_bytes : 0;
   CK(cudaFuncSetAttribute(swk::k_align<kAlignTR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::max<size_t>(prof_smem, 1)));
@@ -1366,7 +1520,7 @@ int sw_align(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix
     if (!d_dir || !d_bnd) return SW_ENOMEM;
     CK(cudaMemcpyAsync(d_jobs + t0, jobs.data() + t0, (size_t)(t1 - t0) * sizeof(swk::AlignJob),
                        cudaMemcpyHostToDevice, st));
-    swk::k_align<kAlignTR><<<t1 - t0, 32, prof_smem, st>>>(db->d_words, d_jobs + t0, t1 - t0, d_prof, (int)prof_smem,
+    swk::k_align<kAlignTR><<<t1 - t0, 32, prof_smem, st>>>(words_dev, d_jobs + t0, t1 - t0, d_prof, (int)prof_smem,
                                                            stride, qlen, m_pad, alpha, beta, d_dir, d_bnd, d_ops,
                                                            d_tmp, d_res + 6 * t0);
     CK(cudaGetLastError());

@@ -43,7 +43,8 @@ def _create(res, offs, lens, gids=None, **kw):
     return sw.Database(res, offs, lens, global_ids=gids, **kw)
 
 
-@pytest.mark.parametrize("case", ["bad_code", "overrun", "neg_len", "bad_gid", "bad_stage"])
+@pytest.mark.parametrize("case", ["bad_code", "overrun", "neg_len", "bad_gid", "bad_stage", "bad_residency",
+                                  "stream_int8", "bad_chunk"])
 def test_db_create_validation(case):
     res = np.array([0, 1, 2, 3, 4, 5], dtype=np.uint8)
     offs = np.array([0, 3], dtype=np.int64)
@@ -60,6 +61,12 @@ def test_db_create_validation(case):
         gids = np.array([0, 1 << 33], dtype=np.int64)
     elif case == "bad_stage":
         kw["first_stage"] = 12
+    elif case == "bad_residency":
+        kw["residency"] = 2
+    elif case == "stream_int8":
+        kw["residency"], kw["first_stage"] = 1, 8
+    elif case == "bad_chunk":
+        kw["residency"], kw["chunk_mb"] = 1, -5
     with pytest.raises(sw.SwError) as ei:
         _create(res, offs, lens, gids, **kw)
     assert ei.value.code == sw.SW_EINVAL
