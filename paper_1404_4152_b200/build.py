@@ -11,6 +11,7 @@ NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler"
            "-diag-suppress", "550"]
 SOURCES = [os.path.join(PKG, "csrc", "sw_api.cu")]
 DEPS = SOURCES + [os.path.join(PKG, "csrc", "sw_kernels.cuh"), os.path.join(PKG, "csrc", "sw_align.cuh"),
+                  os.path.join(PKG, "csrc", "sw_ablation.cuh"),
                   os.path.join(ROOT, "include", "swsearch.h")]
 OUT = os.path.join(PKG, "libswsearch.so")
 

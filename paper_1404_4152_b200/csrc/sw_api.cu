@@ -32,6 +32,7 @@
 #include "../../include/swsearch.h"
 #include "sw_kernels.cuh"
 #include "sw_align.cuh"
+#include "sw_ablation.cuh"
 
 using swk::GroupDesc;
 
@@ -978,6 +979,9 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
     CK(cudaGetLastError());
     return SW_OK;
   };
+  // f4 ablations (measurement switch, not ABI): 1 = InterSP score profile
+  int variant = 0;
+  if (const char* e = getenv("SW_VARIANT")) variant = strcmp(e, "intersp") == 0 ? 1 : 0;
   const int T = tile_rows_env();
   const int nt = threads_env(T == 32 ? 512 : 384);
   void* kern16 = T == 32 ? inter16_kernel_nt<32>(smem, nt) : T == 48 ? inter16_kernel_nt<48>(smem, nt)
@@ -1024,7 +1028,17 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
       cfg.numAttrs = 1;
     }
     cfg.gridDim = dim3(grid);
-    CK(cudaLaunchKernelExC(&cfg, kern16, kargs_inter));
+    if (variant == 1 && !n_groups_dev) {
+      // f4 ablation: InterSP score profile instead of the query profile (SW_VARIANT=intersp)
+      void* kargs_sp[] = {(void*)&words, (void*)&groups, &n_groups_i, &cut, &db->d_query, (void*)&qlen,
+                          (void*)&m_pad, &db->d_matrix, &alpha, &beta, (void*)&limit16, &db->d_scratch, &scols,
+                          &counter_inter, &score_out, &flag_out};
+      cfg.blockDim = dim3(swk::kInterThreads);
+      cfg.dynamicSmemBytes = 0;
+      CK(cudaLaunchKernelExC(&cfg, (void*)swk::k_inter16_sp, kargs_sp));
+    } else {
+      CK(cudaLaunchKernelExC(&cfg, kern16, kargs_inter));
+    }
     nl++;
     return SW_OK;
   };

@@ -1,0 +1,48 @@
+"""f4: the paper's kernel variants rebuilt as ablations (SW_VARIANT) compute the
+same Eq. 1 scores as the oracle, bit-exactly, including tails, long subjects
+(intra-task path beside them) and int32 reruns."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1404_4152_b200 as sw
+from swdata import blosum50, blosum62, matrix32, random_db, stream_key
+from swdata.synth import gen_residues
+
+pytestmark = pytest.mark.gpu
+B62 = matrix32(blosum62())
+B50 = matrix32(blosum50())
+
+
+def _query(m, seed=0):
+    return gen_residues(stream_key(seed, "ablation-query", m), 0, m)
+
+
+@pytest.mark.parametrize("variant", ["intersp"])
+@pytest.mark.parametrize("m", [1, 8, 31, 33, 100, 464, 1100])
+def test_variant_equals_oracle(monkeypatch, variant, m):
+    monkeypatch.setenv("SW_VARIANT", variant)
+    rng = np.random.default_rng(m)
+    lens = np.concatenate([rng.integers(0, 700, 1500), [3000, 4000, 1, 0]])
+    db = random_db(400 + m, lens)
+    q = _query(m, 1)
+    for M, a, b in ((B62, 2, 12), (B50, 0, 3)):
+        with sw.Database.from_synth(db, device=0) as g:
+            r = g.search(q, M, a, b, k=10)
+        ref = oracle.db_scores(q, db, M, a, b)
+        bad = np.nonzero(r.scores != ref)[0]
+        assert bad.size == 0, (variant, m, bad[:5], r.scores[bad[:5]], ref[bad[:5]])
+
+
+@pytest.mark.parametrize("variant", ["intersp"])
+def test_variant_saturation(monkeypatch, variant):
+    monkeypatch.setenv("SW_VARIANT", variant)
+    q = _query(8000, 3)
+    lens = np.array([8000, 300, 4000, 50])
+    db = random_db(9, lens)
+    db.residues[db.offsets[0]:db.offsets[0] + 8000] = q
+    db.residues[db.offsets[2]:db.offsets[2] + 4000] = q[1000:5000]
+    with sw.Database.from_synth(db, device=0) as g:
+        r = g.search(q, B62, 2, 12, k=3)
+    ref = oracle.db_scores(q, db, B62, 2, 12)
+    assert np.array_equal(r.scores, ref) and r.stats["n_rerun32"] >= 1
