@@ -11,6 +11,14 @@
 // column of a per-warp shared-memory table; each query row then reads
 // SP[q_i] with one conflict-free LDS.32 and no PRMT.  The build costs 25 PRMT
 // + 25 STS per column, amortized over the tile's rows.
+//
+// IntraQP (intra-task, query profile, Farrar's striped
+// layout with the lazy-F loop): one warp aligns one subject pair (lo/hi halves
+// of int16x2); lane v holds the contiguous query segment [v*L, (v+1)*L) in
+// registers and all lanes step through their segments together, so the
+// vertical gap (E here) entering a segment is at first assumed 0 and then
+// corrected by a lazy loop that shifts E one lane down and re-walks rows while
+// any lane's incoming E can still raise H.  Replaces the intra-task wavefront.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -139,6 +147,102 @@ k_inter16_sp(const uint2* __restrict__ words, const GroupDesc* __restrict__ grou
     emit_pair(hmax, g, 2 * lane, gd.count, limit, nullptr, score_sorted, flag);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");   // programmatic dependent of k_intra16 (as k_inter16)
+}
+
+// ---------------------------------------------------------------------------
+// IntraQP: one column j of the whole query for one subject pair, striped.
+//   Hold[k] = H(v*L + k, j-1) in, H(v*L + k, j) out;  Fh[k] = F(., j) in, F(., j+1) out
+// ---------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void col_striped(uint32_t (&Hold)[L], uint32_t (&Fh)[L], const int8_t* __restrict__ plo,
+                                            const int8_t* __restrict__ phi, uint32_t na2, uint32_t nb2,
+                                            uint32_t& hmax, int lane) {
+  uint32_t diag = __shfl_up_sync(0xffffffffu, Hold[L - 1], 1);      // H(v*L - 1, j-1)
+  if (lane == 0) diag = 0u;
+  uint32_t ev = 0u;                                                 // E entering the segment: fixed below
+  uint2 a = *reinterpret_cast<const uint2*>(plo), b = *reinterpret_cast<const uint2*>(phi);
+#pragma unroll
+  for (int k = 0; k < L; k++) {
+    const int rr = k & 7;
+    if (rr == 0 && k > 0) {
+      a = *reinterpret_cast<const uint2*>(plo + k);
+      b = *reinterpret_cast<const uint2*>(phi + k);
+    }
+    const uint32_t sub = prmt(rr < 4 ? a.x : a.y, rr < 4 ? b.x : b.y, sel_pair(rr & 3));
+    const uint32_t h = __vimax3_s16x2(__vadd2(diag, sub), ev, Fh[k]);   // >= 0: ev, Fh >= 0
+    diag = Hold[k];
+    Hold[k] = h;
+    const uint32_t hb = __vadd2(h, nb2);
+    Fh[k] = __viaddmax_s16x2_relu(Fh[k], na2, hb);
+    ev = __viaddmax_s16x2_relu(ev, na2, hb);
+    hmax = __vmaxs2(hmax, h);
+  }
+  // lazy loop: E leaving lane v-1's segment enters lane v's first row
+  for (int wrap = 0; wrap < 32; wrap++) {
+    ev = __shfl_up_sync(0xffffffffu, ev, 1);
+    if (lane == 0) ev = 0u;
+    bool live = true;
+#pragma unroll
+    for (int k = 0; k < L; k++) {
+      // can the incoming E still change H (or the gaps derived from it) at this row?
+      // Not if E <= max(H - beta, 0): gaps are clamped at 0, so a
+      // zero E is inert (Farrar's test on saturating unsigned lanes).
+      const uint32_t hb_old = __vmaxs2(__vadd2(Hold[k], nb2), 0u);
+      if (!__any_sync(0xffffffffu, __vcmpgts2(ev, hb_old) != 0u)) { live = false; break; }
+      Hold[k] = __vmaxs2(Hold[k], ev);
+      hmax = __vmaxs2(hmax, Hold[k]);
+      const uint32_t hb = __vadd2(Hold[k], nb2);
+      Fh[k] = __vmaxs2(Fh[k], hb);
+      ev = __viaddmax_s16x2_relu(ev, na2, hb);
+    }
+    if (!live) break;
+  }
+}
+
+// IntraQP ablation of k_intra16: pair items of the long groups, striped.
+template <int L, bool SMEM>
+__global__ void __launch_bounds__(kInterThreads, 1)
+k_intra16_qp(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups, int cut,
+             const int8_t* __restrict__ gprof, int stride, int alpha, int beta, int limit,
+             int* __restrict__ counter, int* __restrict__ score_sorted, uint8_t* __restrict__ flag) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  extern __shared__ __align__(16) int8_t sprof[];
+  __shared__ int s_split;
+  if (threadIdx.x == 0) s_split = split_groups(groups, n_groups, cut);
+  __syncthreads();
+  const int split = s_split;
+  const int n_items = (n_groups - split) * 32;
+  if (n_items <= 0) return;
+  if (SMEM) load_profile_smem(sprof, gprof, stride);
+  const int8_t* prof = prof_base<SMEM>(gprof);
+  const int lane = threadIdx.x & 31;
+  const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
+  const int8_t* pr = prof + lane * L;                                // this lane's query segment
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(counter, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    const int g = n_groups - 1 - item / 32;
+    const int p = 31 - item % 32;
+    const GroupDesc gd = groups[g];
+    if (2 * p >= gd.count) continue;
+    const uint2* pw = words + gd.base + p;
+    const int ncols = gd.ncols, nwords = (ncols + kResPerWord - 1) / kResPerWord;
+    uint32_t Hold[L], Fh[L], hmax = 0u;
+#pragma unroll
+    for (int k = 0; k < L; k++) { Hold[k] = 0u; Fh[k] = 0u; }
+    uint2 w = make_uint2(kDummyWord, kDummyWord);
+    for (int j = 0; j < ncols; j++) {
+      const int sh = res_shift(j);
+      if (sh == 0) w = j / kResPerWord < nwords ? __ldg(pw + (long long)(j / kResPerWord) * 32) : w;
+      col_striped<L>(Hold, Fh, pr + ((w.x >> sh) & 31u) * stride, pr + ((w.y >> sh) & 31u) * stride, na2, nb2,
+                     hmax, lane);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hmax = __vmaxs2(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+    if (lane == 0) emit_pair(hmax, g, 2 * p, gd.count, limit, nullptr, score_sorted, flag);
+  }
 }
 
 }  // namespace swk

@@ -135,6 +135,8 @@ struct sw_db {
   int* d_len_sorted = nullptr;    // sorted position -> length
   long long* d_gid = nullptr;     // input index -> global id (nullptr: identity)
   int* d_inv = nullptr;           // input index -> sorted position (built on the first sw_align)
+  int8_t* d_prof_qp = nullptr;    // f4 IntraQP ablation: profile with rows of 32*L bytes
+  size_t prof_qp_cap = 0;
   void* aw[10] = {};              // sw_align workspace (grow-only): idx, jobs, res, q, M, prof, dir, bnd, ops, tmp
   size_t aw_cap[10] = {};
 
@@ -231,7 +233,7 @@ static void free_db(sw_db* db) {
                   db->d_prof_b, db->d_prof2, db->d_score_sorted2, db->d_flag_b, db->d_scratch_intra,
                   db->d_counters, db->d_hist, db->d_sel,
                   db->d_topk_ids, db->d_topk_scores, db->d_cub, db->d_inv, db->d_chunk[0], db->d_chunk[1],
-                  db->d_stream_cnt};
+                  db->d_stream_cnt, db->d_prof_qp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (void* p : db->aw)
@@ -979,9 +981,34 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
     CK(cudaGetLastError());
     return SW_OK;
   };
-  // f4 ablations (measurement switch, not ABI): 1 = InterSP score profile
+  // f4 ablations (measurement switch, not ABI): 1 = InterSP score profile,
+  // 2 = IntraQP striped intra-task kernel (queries up to 2,048 rows)
   int variant = 0;
-  if (const char* e = getenv("SW_VARIANT")) variant = strcmp(e, "intersp") == 0 ? 1 : 0;
+  if (const char* e = getenv("SW_VARIANT")) variant = strcmp(e, "intersp") == 0 ? 1 : strcmp(e, "intraqp") == 0 ? 2 : 0;
+  const int qp_L = ((m_pad + 31) / 32 + 7) / 8 * 8;                  // rows per lane, multiple of 8
+  const int qp_stride = 32 * qp_L + 8;
+  const size_t qp_bytes = ((size_t)swk::kProfRows * qp_stride + 15) / 16 * 16;
+  void* kintra_qp = nullptr;
+  if (variant == 2 && qp_L <= 64) {
+    void* pq = db->d_prof_qp;
+    int rc = ensure(&pq, &db->prof_qp_cap, qp_bytes);
+    db->d_prof_qp = (int8_t*)pq;
+    if (rc) return rc;
+    swk::k_profile<<<64, 256, 0, st>>>(db->d_query, qlen, db->d_matrix, db->d_prof_qp, qp_stride);
+    CK(cudaGetLastError());
+    nl++;
+    switch (qp_L) {
+      case 8: kintra_qp = (void*)swk::k_intra16_qp<8, true>; break;
+      case 16: kintra_qp = (void*)swk::k_intra16_qp<16, true>; break;
+      case 24: kintra_qp = (void*)swk::k_intra16_qp<24, true>; break;
+      case 32: kintra_qp = (void*)swk::k_intra16_qp<32, true>; break;
+      case 40: kintra_qp = (void*)swk::k_intra16_qp<40, true>; break;
+      case 48: kintra_qp = (void*)swk::k_intra16_qp<48, true>; break;
+      case 56: kintra_qp = (void*)swk::k_intra16_qp<56, true>; break;
+      default: kintra_qp = (void*)swk::k_intra16_qp<64, true>; break;
+    }
+    CK(cudaFuncSetAttribute(kintra_qp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qp_bytes));
+  }
   const int T = tile_rows_env();
   const int nt = threads_env(T == 32 ? 512 : 384);
   void* kern16 = T == 32 ? inter16_kernel_nt<32>(smem, nt) : T == 48 ? inter16_kernel_nt<48>(smem, nt)
@@ -1022,7 +1049,14 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
       // hold SMs the inter-task kernel could use
       const int64_t items = (int64_t)(n_groups_dev ? n_groups_i : n_long_r) * 32;
       const int grid_intra = (int)std::max<int64_t>(1, std::min<int64_t>(grid, (items + 11) / 12));
-      CK(cudaLaunchKernel(kintra, dim3(grid_intra), dim3(swk::kInterThreads), kargs_intra, smem_bytes, st));
+      if (kintra_qp && !n_groups_dev) {
+        // f4 ablation: striped intra-task kernel (IntraQP) for the pair items
+        void* kargs_qp[] = {(void*)&words, (void*)&groups, &n_groups_i, &cut, &db->d_prof_qp, (void*)&qp_stride,
+                            &alpha, &beta, (void*)&limit16, &counter_intra, &score_out, &flag_out};
+        CK(cudaLaunchKernel(kintra_qp, dim3(grid_intra), dim3(swk::kInterThreads), kargs_qp, qp_bytes, st));
+      } else {
+        CK(cudaLaunchKernel(kintra, dim3(grid_intra), dim3(swk::kInterThreads), kargs_intra, smem_bytes, st));
+      }
       nl++;
       cfg.attrs = pdl;
       cfg.numAttrs = 1;

@@ -18,10 +18,12 @@ def _query(m, seed=0):
     return gen_residues(stream_key(seed, "ablation-query", m), 0, m)
 
 
-@pytest.mark.parametrize("variant", ["intersp"])
+@pytest.mark.parametrize("variant", ["intersp", "intraqp"])
 @pytest.mark.parametrize("m", [1, 8, 31, 33, 100, 464, 1100])
 def test_variant_equals_oracle(monkeypatch, variant, m):
     monkeypatch.setenv("SW_VARIANT", variant)
+    if variant == "intraqp":
+        monkeypatch.setenv("SW_LONG_COLS", "1")           # every group through the (striped) intra-task path
     rng = np.random.default_rng(m)
     lens = np.concatenate([rng.integers(0, 700, 1500), [3000, 4000, 1, 0]])
     db = random_db(400 + m, lens)
@@ -34,15 +36,20 @@ def test_variant_equals_oracle(monkeypatch, variant, m):
         assert bad.size == 0, (variant, m, bad[:5], r.scores[bad[:5]], ref[bad[:5]])
 
 
-@pytest.mark.parametrize("variant", ["intersp"])
-def test_variant_saturation(monkeypatch, variant):
+@pytest.mark.parametrize("variant,m", [("intersp", 8000), ("intraqp", 2000)])
+def test_variant_saturation(monkeypatch, variant, m):
+    """Planted copies whose self-score exceeds int16: flagged, rerun in int32, exact."""
     monkeypatch.setenv("SW_VARIANT", variant)
-    q = _query(8000, 3)
-    lens = np.array([8000, 300, 4000, 50])
+    monkeypatch.setenv("SW_LONG_COLS", "1")
+    q = _query(m, 3)
+    M = B62.copy()
+    for c in range(20):
+        M[c, c] = 100                                     # self-score ~ 100 m > 32767 at m = 2000
+    lens = np.array([m, 300, m // 2, 50])
     db = random_db(9, lens)
-    db.residues[db.offsets[0]:db.offsets[0] + 8000] = q
-    db.residues[db.offsets[2]:db.offsets[2] + 4000] = q[1000:5000]
+    db.residues[db.offsets[0]:db.offsets[0] + m] = q
+    db.residues[db.offsets[2]:db.offsets[2] + m // 2] = q[m // 8:m // 8 + m // 2]
     with sw.Database.from_synth(db, device=0) as g:
-        r = g.search(q, B62, 2, 12, k=3)
-    ref = oracle.db_scores(q, db, B62, 2, 12)
+        r = g.search(q, M, 2, 12, k=3)
+    ref = oracle.db_scores(q, db, M, 2, 12)
     assert np.array_equal(r.scores, ref) and r.stats["n_rerun32"] >= 1

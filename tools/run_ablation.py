@@ -24,7 +24,7 @@ print(json.dumps({"ms_first_pass": round(t, 3), "gcups_first_pass": round(cells 
 ''' % ROOT
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="C2,C4")
-ap.add_argument("--variants", default="base,intersp")
+ap.add_argument("--variants", default="base,intersp,intra,intraqp")
 ap.add_argument("--json", default=None)
 a = ap.parse_args()
 rows = []
@@ -32,8 +32,11 @@ for cfgname in a.configs.split(","):
     for v in a.variants.split(","):
         env = dict(os.environ)
         env.pop("SW_VARIANT", None)
-        if v != "base":
+        env.pop("SW_LONG_COLS", None)
+        if v in ("intersp", "intraqp"):
             env["SW_VARIANT"] = v
+        if v in ("intra", "intraqp"):                    # every group through the intra-task path
+            env["SW_LONG_COLS"] = "1"
         out = subprocess.run([sys.executable, "-c", code, cfgname], env=env, capture_output=True, text=True)
         try:
             res = json.loads(out.stdout.strip().splitlines()[-1])
