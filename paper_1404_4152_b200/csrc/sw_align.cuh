@@ -53,112 +53,156 @@ __device__ __forceinline__ bool better(int h, int j, int i, int bh, int bj, int 
   return h > bh || (h == bh && (j < bj || (j == bj && i < bi)));
 }
 
+constexpr int kAlignWarps = 8;       // warps per hit: one 32*TR-row band each, pipelined along the columns
+constexpr int kRing = 128;           // columns of (H, E) in flight between neighbouring warps (shared memory)
+
 // res[t*6 + ...] = score, q_begin, q_end, s_begin, s_end, n_ops
+//
+// One CTA of kAlignWarps warps per hit.  The query rows are cut into bands of
+// 32*TR rows; in round r warp w fills band r*W + w over all columns with the
+// lane wavefront, taking the row above its band from warp w-1 through a
+// shared-memory ring (or, for warp 0, from the previous round's last warp
+// through global memory) and running ~64 columns behind it.
 template <int TR>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(32 * kAlignWarps)
 k_align(const uint2* __restrict__ words, const AlignJob* __restrict__ jobs, int n_jobs,
         const int8_t* __restrict__ prof, int prof_smem, int stride, int m, int m_pad, int alpha, int beta,
         uint32_t* __restrict__ dir, int2* __restrict__ bnd, char* __restrict__ ops_out,
         char* __restrict__ ops_tmp, int* __restrict__ res) {
   const int t = blockIdx.x;
   if (t >= n_jobs) return;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const AlignJob J = jobs[t];
   const int n = J.n;
   const uint32_t* wp = reinterpret_cast<const uint32_t*>(words + J.word0) + J.half;   // word w at wp[64 w]
   uint32_t* D = dir + J.dir;
   int2* B = bnd + J.bnd;
   int best = 0, bj = 0x7fffffff, bi = 0x7fffffff;
+  int stalled = 0;
+  __shared__ int2 ring[kAlignWarps - 1][kRing];
+  __shared__ int s_stalled;
+  if (threadIdx.x == 0) s_stalled = 0;
+  __shared__ volatile int prod[kAlignWarps], cons[kAlignWarps];
+  __shared__ int s_best[kAlignWarps][3];
+  __shared__ int s_nops;
   // the int8 query profile is staged in shared memory (prof_smem bytes, 0 = read through L1)
   extern __shared__ __align__(16) int8_t s_prof[];
   const int8_t* P = prof;
   if (prof_smem) {
     const uint4* src = reinterpret_cast<const uint4*>(prof);
     uint4* dst = reinterpret_cast<uint4*>(s_prof);
-    for (int k = lane; k < prof_smem / 16; k += 32) dst[k] = __ldg(src + k);
-    __syncwarp();
+    for (int k = threadIdx.x; k < prof_smem / 16; k += blockDim.x) dst[k] = __ldg(src + k);
     P = s_prof;
   }
-  int pass = 0;
-  for (int base = 0; n > 0 && base < m_pad; base += 32 * TR, pass++) {
-    const int nact = min(32, (m_pad - base) / TR);
-    const bool first = base == 0, last = base + 32 * TR >= m_pad;
-    const int2* gin = B + (long long)(pass & 1) * n;            // written by the previous pass
-    int2* gout = B + (long long)((pass + 1) & 1) * n;
-    const int i0 = base + lane * TR;
-    const int8_t* pr = P + i0;
-    int Hc[TR], Fc[TR];                                          // H(i, j-1), F(i, j-1)
+  const int band_rows = 32 * TR;
+  const int n_bands = (m_pad + band_rows - 1) / band_rows;
+  for (int round = 0; n > 0 && round * kAlignWarps < n_bands; round++) {
+    __syncthreads();                                             // the previous round is done with the rings
+    if (lane == 0) { prod[warp] = 0; cons[warp] = 0; }
+    __syncthreads();                                             // also: profile staged, previous round's gout written
+    const int band = round * kAlignWarps + warp;
+    if (band < n_bands) {
+      const int base = band * band_rows;
+      const int nact = min(32, (m_pad - base) / TR);
+      const bool first = band == 0, last = band == n_bands - 1;
+      const bool from_ring = !first && warp > 0, to_ring = !last && warp < kAlignWarps - 1;
+      const int2* gin = B + (long long)(round & 1) * n;          // written by the previous round's last warp
+      int2* gout = B + (long long)((round + 1) & 1) * n;
+      const int i0 = base + lane * TR;
+      const int8_t* pr = P + i0;
+      int Hc[TR], Fc[TR];                                        // H(i, j-1), F(i, j-1)
 #pragma unroll
-    for (int r = 0; r < TR; r++) { Hc[r] = 0; Fc[r] = 0; }        // H(i,0) = F(i,0) = 0
-    int h_out = 0, e_out = 0, hdiag = 0;                         // hdiag = H(i0-1, j-1)
-    uint32_t c_out = 0;                                          // residue of the column this lane just did
-    // lane 0's per-step inputs (residue of column s, boundary row of column s)
-    // are fetched 32 steps at a time, one block ahead, and handed over by SHFL
-    auto fetch = [&](int sb, uint32_t& rc, int2& gv) {
-      const int c = sb + lane;
-      rc = c < n ? (__ldg(wp + 64 * (c / 6)) >> (5 * (c % 6))) & 31u : 0u;
-      gv = (!first && c < n) ? gin[c] : make_int2(0, 0);
-    };
-    uint32_t rc_cur, rc_nxt;
-    int2 gv_cur, gv_nxt;
-    fetch(0, rc_cur, gv_cur);
-    fetch(32, rc_nxt, gv_nxt);
-    const int nsteps = n + nact - 1;
-    for (int sb = 0; sb < nsteps; sb += 32) {
-#pragma unroll 1
-      for (int tt = 0; tt < 32; tt++) {
-        const int s = sb + tt;
-        if (s >= nsteps) break;
-        int h_in = __shfl_up_sync(0xffffffffu, h_out, 1);
-        int e_in = __shfl_up_sync(0xffffffffu, e_out, 1);
-        uint32_t c = __shfl_up_sync(0xffffffffu, c_out, 1);
-        const uint32_t c0 = __shfl_sync(0xffffffffu, rc_cur, tt);
-        const int g0x = __shfl_sync(0xffffffffu, gv_cur.x, tt);
-        const int g0y = __shfl_sync(0xffffffffu, gv_cur.y, tt);
-        const int j = s - lane;
-        if (lane == 0) {                                         // row base-1 of column j, residue s_j
-          h_in = g0x;
-          e_in = g0y;
-          c = c0;
-        }
-        if (lane < nact && j >= 0 && j < n) {
-          const uint2 pv = *reinterpret_cast<const uint2*>(pr + c * stride);
-          int hu = h_in, eu = e_in, dg = hdiag;
-          uint32_t nib = 0;
-#pragma unroll
-          for (int r = 0; r < TR; r++) {
-            const int sub = (int)(int8_t)(((r < 4 ? pv.x : pv.y) >> (8 * (r & 3))) & 0xffu);
-            const int G = dg + sub;                                // H(i-1,j-1) + fsbt(q_i, s_j)
-            const int eo = hu - beta, ee = eu - alpha;
-            const int E = max(ee, eo);                             // E(i,j)
-            const int fo = Hc[r] - beta, fe = Fc[r] - alpha;
-            const int F = max(fe, fo);                             // F(i,j)
-            const int H = max(max(0, G), max(E, F));
-            const uint32_t src = H == 0 ? 0u : H == G ? 1u : H == E ? 2u : 3u;
-            nib |= (src | (ee > eo ? 4u : 0u) | (fe > fo ? 8u : 0u)) << (4 * r);
-            const int i = i0 + r;
-            if (i < m && better(H, j, i, best, bj, bi)) { best = H; bj = j; bi = i; }
-            dg = Hc[r];                                            // H(i, j-1): diagonal of row i+1
-            Hc[r] = H;
-            Fc[r] = F;
-            hu = H;
-            eu = E;
+      for (int r = 0; r < TR; r++) { Hc[r] = 0; Fc[r] = 0; }      // H(i,0) = F(i,0) = 0
+      int h_out = 0, e_out = 0, hdiag = 0;                       // hdiag = H(i0-1, j-1)
+      uint32_t c_out = 0;                                        // residue of the column this lane just did
+      const int nsteps = n + nact - 1;
+      for (int sb = 0; sb < nsteps; sb += 32) {
+        // lane 0's inputs for steps sb..sb+31: residue of column sb+k and the row above the band
+        const int c = sb + lane;
+        const uint32_t rc_cur = c < n ? (__ldg(wp + 64 * (c / 6)) >> (5 * (c % 6))) & 31u : 0u;
+        int2 gv_cur = make_int2(0, 0);
+        if (from_ring) {
+          const int need = min(n, sb + 32);
+          for (int spin = 0; prod[warp - 1] < need; spin++) {
+            if (spin > (1 << 24)) { stalled = 1; break; }         // never expected: reported, not hung
+            __nanosleep(20);
           }
-          D[(long long)(i0 / TR) * n + j] = nib;
-          if (!last && lane == nact - 1) gout[j] = make_int2(hu, eu);
-          h_out = hu;
-          e_out = eu;
-          c_out = c;
-          hdiag = h_in;                                            // H(i0-1, j) is the next column's diagonal
+          __threadfence_block();
+          if (c < n) gv_cur = ring[warp - 1][c % kRing];
+          __syncwarp();
+          if (lane == 0) cons[warp - 1] = need;                   // these ring slots may be reused
+        } else if (!first && c < n) {
+          gv_cur = __ldcg(gin + c);
+        }
+        if (to_ring) {                                           // this block writes columns up to sb
+          for (int spin = 0; cons[warp] < sb + 1 - kRing; spin++) {
+            if (spin > (1 << 24)) { stalled = 1; break; }
+            __nanosleep(20);
+          }
+        }
+#pragma unroll 1
+        for (int tt = 0; tt < 32; tt++) {
+          const int s = sb + tt;
+          if (s >= nsteps) break;
+          int h_in = __shfl_up_sync(0xffffffffu, h_out, 1);
+          int e_in = __shfl_up_sync(0xffffffffu, e_out, 1);
+          uint32_t cc = __shfl_up_sync(0xffffffffu, c_out, 1);
+          const uint32_t c0 = __shfl_sync(0xffffffffu, rc_cur, tt);
+          const int g0x = __shfl_sync(0xffffffffu, gv_cur.x, tt);
+          const int g0y = __shfl_sync(0xffffffffu, gv_cur.y, tt);
+          const int j = s - lane;
+          if (lane == 0) {                                       // row base-1 of column j, residue s_j
+            h_in = g0x;
+            e_in = g0y;
+            cc = c0;
+          }
+          if (lane < nact && j >= 0 && j < n) {
+            const uint2 pv = *reinterpret_cast<const uint2*>(pr + cc * stride);
+            int hu = h_in, eu = e_in, dg = hdiag;
+            uint32_t nib = 0;
+#pragma unroll
+            for (int r = 0; r < TR; r++) {
+              const int sub = (int)(int8_t)(((r < 4 ? pv.x : pv.y) >> (8 * (r & 3))) & 0xffu);
+              const int G = dg + sub;                              // H(i-1,j-1) + fsbt(q_i, s_j)
+              const int eo = hu - beta, ee = eu - alpha;
+              const int E = max(ee, eo);                           // E(i,j)
+              const int fo = Hc[r] - beta, fe = Fc[r] - alpha;
+              const int F = max(fe, fo);                           // F(i,j)
+              const int H = max(max(0, G), max(E, F));
+              const uint32_t src = H == 0 ? 0u : H == G ? 1u : H == E ? 2u : 3u;
+              nib |= (src | (ee > eo ? 4u : 0u) | (fe > fo ? 8u : 0u)) << (4 * r);
+              const int i = i0 + r;
+              if (i < m && better(H, j, i, best, bj, bi)) { best = H; bj = j; bi = i; }
+              dg = Hc[r];                                          // H(i, j-1): diagonal of row i+1
+              Hc[r] = H;
+              Fc[r] = F;
+              hu = H;
+              eu = E;
+            }
+            D[(long long)(i0 / TR) * n + j] = nib;
+            if (lane == nact - 1 && !last) {
+              if (to_ring) ring[warp][j % kRing] = make_int2(hu, eu);
+              else gout[j] = make_int2(hu, eu);
+            }
+            h_out = hu;
+            e_out = eu;
+            c_out = cc;
+            hdiag = h_in;                                          // H(i0-1, j) is the next column's diagonal
+          }
+        }
+        if (to_ring) {                                           // publish columns 0 .. min(sb, n-1)
+          __threadfence_block();
+          __syncwarp();
+          if (lane == 0) prod[warp] = min(n, sb + 1);
         }
       }
-      rc_cur = rc_nxt;
-      gv_cur = gv_nxt;
-      fetch(sb + 64, rc_nxt, gv_nxt);
+      if (to_ring && lane == 0) {
+        __threadfence_block();
+        prod[warp] = n;
+      }
     }
-    __syncwarp();
   }
-  // end cell: lexicographic (max H, min j, min i) over the warp
+  // end cell: lexicographic (max H, min j, min i) over the CTA
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const int h2 = __shfl_xor_sync(0xffffffffu, best, o);
@@ -166,48 +210,77 @@ k_align(const uint2* __restrict__ words, const AlignJob* __restrict__ jobs, int 
     const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
     if (better(h2, j2, i2, best, bj, bi)) { best = h2; bj = j2; bi = i2; }
   }
-  __syncwarp();
-  __shared__ int s_nops;
+  if (lane == 0) { s_best[warp][0] = best; s_best[warp][1] = bj; s_best[warp][2] = bi; }
+  if (stalled) s_stalled = 1;
+  __syncthreads();                                               // all direction words written and visible
+  if (warp != 0) return;
+  best = s_best[0][0]; bj = s_best[0][1]; bi = s_best[0][2];
+  for (int w = 1; w < kAlignWarps; w++)
+    if (better(s_best[w][0], s_best[w][1], s_best[w][2], best, bj, bi)) {
+      best = s_best[w][0]; bj = s_best[w][1]; bi = s_best[w][2];
+    }
+  // walk back (warp 0, all lanes in step): the direction words of row blocks
+  // {rb, rb-1} x columns [cj-15, cj] sit in the lanes' registers (lane = 16*dr + dc)
+  // and are re-loaded only when the walk leaves that window.
+  char* tmp = ops_tmp + J.tmp;
+  int i = bi, j = bj, k = 0, state = 0;                          // 0 = H, 1 = E (vertical), 2 = F (horizontal)
+  bool bad = s_stalled != 0;
+  if (best > 0 && !bad) {
+    int wrb = -100, wcj = -100;
+    uint32_t win = 0u;
+    for (;;) {
+      if (state == 0 && (i < 0 || j < 0)) break;
+      if (i < 0 || j < 0 || k > m + n) { bad = true; break; }    // inconsistent directions: reported, not hung
+      const int rb = i / TR;
+      if (rb > wrb || rb < wrb - 1 || j > wcj || j < wcj - 15) {
+        wrb = rb;
+        wcj = j;
+        const int lr = wrb - (lane >> 4), lc = wcj - 15 + (lane & 15);
+        win = (lr >= 0 && lc >= 0) ? __ldcg(D + (long long)lr * n + lc) : 0u;
+      }
+      const uint32_t w = __shfl_sync(0xffffffffu, win, 16 * (wrb - rb) + (j - (wcj - 15)));
+      const uint32_t nib = (w >> (4 * (i % TR))) & 15u;
+      if (state == 0) {
+        const uint32_t src = nib & 3u;
+        if (src == 0u) break;
+        if (src == 1u) { if (lane == 0) tmp[k] = 'M'; k++; i--; j--; }
+        else state = src == 2u ? 1 : 2;
+      } else if (state == 1) {
+        if (lane == 0) tmp[k] = 'I';
+        k++;
+        i--;
+        state = (nib & 4u) ? 1 : 0;
+      } else {
+        if (lane == 0) tmp[k] = 'D';
+        k++;
+        j--;
+        state = (nib & 8u) ? 2 : 0;
+      }
+    }
+  }
   if (lane == 0) {
     int* R = res + 6 * t;
-    if (best == 0) {
+    if (bad) {
+      R[0] = -1;                                                 // the host turns this into SW_EINTERNAL
+      R[1] = R[2] = R[3] = R[4] = R[5] = 0;
+      k = 0;
+    } else if (best == 0) {
       R[0] = R[1] = R[2] = R[3] = R[4] = R[5] = 0;
-      s_nops = 0;
+      k = 0;
     } else {
-      char* tmp = ops_tmp + J.tmp;
-      int i = bi, j = bj, k = 0, state = 0;                      // 0 = H, 1 = E (vertical), 2 = F (horizontal)
-      for (;;) {
-        if (state == 0 && (i < 0 || j < 0)) break;
-        const uint32_t nib = (__ldcg(D + (long long)(i / TR) * n + j) >> (4 * (i % TR))) & 15u;
-        if (state == 0) {
-          const uint32_t src = nib & 3u;
-          if (src == 0u) break;
-          if (src == 1u) { tmp[k++] = 'M'; i--; j--; }
-          else state = src == 2u ? 1 : 2;
-        } else if (state == 1) {
-          tmp[k++] = 'I';
-          i--;
-          state = (nib & 4u) ? 1 : 0;
-        } else {
-          tmp[k++] = 'D';
-          j--;
-          state = (nib & 8u) ? 2 : 0;
-        }
-      }
       R[0] = best;
       R[1] = i + 1;
       R[2] = bi + 1;
       R[3] = j + 1;
       R[4] = bj + 1;
       R[5] = k;
-      s_nops = k;
     }
+    s_nops = k;
   }
   __syncwarp();
   const int nops = s_nops;
-  const char* tmp = ops_tmp + J.tmp;
   char* out = ops_out + J.ops;
-  for (int k = lane; k < nops; k += 32) out[k] = tmp[nops - 1 - k];
+  for (int q = lane; q < nops; q += 32) out[q] = tmp[nops - 1 - q];
 }
 
 }  // namespace swk

@@ -1568,7 +1568,7 @@ int sw_align(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix
     if (!d_dir || !d_bnd) return SW_ENOMEM;
     CK(cudaMemcpyAsync(d_jobs + t0, jobs.data() + t0, (size_t)(t1 - t0) * sizeof(swk::AlignJob),
                        cudaMemcpyHostToDevice, st));
-    swk::k_align<kAlignTR><<<t1 - t0, 32, prof_smem, st>>>(words_dev, d_jobs + t0, t1 - t0, d_prof, (int)prof_smem,
+    swk::k_align<kAlignTR><<<t1 - t0, 32 * swk::kAlignWarps, prof_smem, st>>>(words_dev, d_jobs + t0, t1 - t0, d_prof, (int)prof_smem,
                                                            stride, qlen, m_pad, alpha, beta, d_dir, d_bnd, d_ops,
                                                            d_tmp, d_res + 6 * t0);
     CK(cudaGetLastError());
@@ -1580,6 +1580,10 @@ int sw_align(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix
   CK(cudaMemcpyAsync(res.data(), d_res, res.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(ops, d_ops, (size_t)need, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  for (int32_t t = 0; t < n; t++)
+    if (res[6 * t] < 0)
+      return fail(SW_EINTERNAL, "sw_align: traceback of subject %lld failed (device pipeline stalled or "
+                  "inconsistent direction codes)", (long long)subjects[t]);
   for (int32_t t = 0; t < n; t++) {
     sw_alignment& a = out[t];
     a.subject = subjects[t];

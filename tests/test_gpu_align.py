@@ -72,7 +72,7 @@ def test_random_lengths_every_subject():
         _check(db, _query(m), B62, 2, 12)
 
 
-@pytest.mark.parametrize("m", [100, 464, 513, 1000])
+@pytest.mark.parametrize("m", [100, 464, 513, 1000, 2100, 4200])
 def test_planted_near_copies(m):
     """Near-copies of the query (80% identity, indels: the C4 planting model)
     give long gapped alignments crossing lane, pass and row-block edges."""
