@@ -73,13 +73,14 @@ int threads_env(int def) {
 }
 
 template <int T, int NT>
-void* inter16_kernel(bool smem) {
+void* inter16_kernel(bool smem, bool big) {
+  if (big) return smem ? (void*)swk::k_inter16<T, true, NT, true> : (void*)swk::k_inter16<T, false, NT, true>;
   return smem ? (void*)swk::k_inter16<T, true, NT> : (void*)swk::k_inter16<T, false, NT>;
 }
 
 template <int T>
-void* inter16_kernel_nt(bool smem, int nt) {
-  return nt == 512 ? inter16_kernel<T, 512>(smem) : inter16_kernel<T, 384>(smem);
+void* inter16_kernel_nt(bool smem, int nt, bool big) {
+  return nt == 512 ? inter16_kernel<T, 512>(smem, big) : inter16_kernel<T, 384>(smem, big);
 }
 constexpr int kMaxSmemProfile = 200 * 1024;
 
@@ -135,6 +136,8 @@ struct sw_db {
   int* d_len_sorted = nullptr;    // sorted position -> length
   long long* d_gid = nullptr;     // input index -> global id (nullptr: identity)
   int* d_inv = nullptr;           // input index -> sorted position (built on the first sw_align)
+  uint2* d_big = nullptr;         // boundary slabs of the inter-task groups wider than a warp's slab
+  size_t big_cap = 0;
   int8_t* d_prof_qp = nullptr;    // f4 IntraQP ablation: profile with rows of 32*L bytes
   size_t prof_qp_cap = 0;
   void* aw[10] = {};              // sw_align workspace (grow-only): idx, jobs, res, q, M, prof, dir, bnd, ops, tmp
@@ -233,7 +236,7 @@ static void free_db(sw_db* db) {
                   db->d_prof_b, db->d_prof2, db->d_score_sorted2, db->d_flag_b, db->d_scratch_intra,
                   db->d_counters, db->d_hist, db->d_sel,
                   db->d_topk_ids, db->d_topk_scores, db->d_cub, db->d_inv, db->d_chunk[0], db->d_chunk[1],
-                  db->d_stream_cnt, db->d_prof_qp};
+                  db->d_stream_cnt, db->d_prof_qp, db->d_big};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (void* p : db->aw)
@@ -963,10 +966,42 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
     int64_t c;
     const int64_t n_warps = (int64_t)db->num_sms * (swk::kInterThreads / 32);
     if (db->long_threshold > 0) c = db->long_threshold;
-    else if (db->long_threshold == 0) c = std::max<int64_t>(256, db->sum_len / (64 * std::max<int64_t>(n_warps, 1)));
+    else if (db->long_threshold == 0) c = std::max<int64_t>(128, db->sum_len / (64 * std::max<int64_t>(n_warps, 1)));
     else c = INT64_MAX;
     if (const char* e = getenv("SW_LONG_COLS")) c = atoll(e);
-    cut = (int)std::min<int64_t>(c, db->scratch_cols);
+    cut = (int)std::min<int64_t>(c, INT32_MAX);
+  }
+  // Groups wider than a warp's boundary slab (scratch_cols) stay inter-task with
+  // a slab of their own ("big" items: they are the first items of the
+  // longest-first queue); at most kMaxBig of them and kBigBytes of slabs, the
+  // rest of the widest groups go to the intra-task kernel.
+  long long big_cols = 0;
+  int n_big = 0;
+  {
+    constexpr int64_t kMaxBig = 2048;
+    constexpr int64_t kBigBytes = 8LL << 30;
+    const auto& gc = db->group_ncols;
+    const int64_t b0 = std::upper_bound(gc.begin(), gc.end(), (int)db->scratch_cols) - gc.begin();
+    int64_t b1 = std::upper_bound(gc.begin(), gc.end(), cut) - gc.begin();   // inter-task groups: [0, b1)
+    if (b1 > b0) {
+      b1 = std::min<int64_t>(b1, b0 + kMaxBig);
+      while (b1 > b0 && (b1 - b0) * (int64_t)(gc[b1 - 1] + swk::kResPerWord) * 32 * (int64_t)sizeof(uint2) > kBigBytes) b1--;
+      cut = b1 > b0 ? gc[b1 - 1] : (int)db->scratch_cols;
+      if (b1 < (int64_t)gc.size() && gc[b1] == cut) {          // keep the split on a column count boundary
+        while (b1 > b0 && gc[b1 - 1] == cut) b1--;
+        cut = b1 > b0 ? gc[b1 - 1] : (int)db->scratch_cols;
+      }
+      n_big = (int)(b1 - b0);
+      big_cols = n_big ? (long long)cut + 2 * swk::kResPerWord : 0;
+      if (n_big) {
+        void* pb = db->d_big;
+        int rc = ensure(&pb, &db->big_cap, (size_t)n_big * big_cols * 32 * sizeof(uint2));
+        db->d_big = (uint2*)pb;
+        if (rc) return rc;
+      }
+    } else {
+      cut = (int)std::min<int64_t>(cut, db->scratch_cols);
+    }
   }
   const int n_long = (int)(db->group_ncols.end() -
                            std::upper_bound(db->group_ncols.begin(), db->group_ncols.end(), cut));
@@ -1011,8 +1046,9 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   }
   const int T = tile_rows_env();
   const int nt = threads_env(T == 32 ? 512 : 384);
-  void* kern16 = T == 32 ? inter16_kernel_nt<32>(smem, nt) : T == 48 ? inter16_kernel_nt<48>(smem, nt)
-               : inter16_kernel_nt<64>(smem, nt);
+  // the BIG instantiation (per-item slab choice) only when wide groups stay inter-task
+  void* kern16 = T == 32 ? inter16_kernel_nt<32>(smem, nt, n_big > 0) : T == 48 ? inter16_kernel_nt<48>(smem, nt, n_big > 0)
+               : inter16_kernel_nt<64>(smem, nt, n_big > 0);
   CK(cudaFuncSetAttribute(kern16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_bytes, 1)));
   const int intra_tr = m_pad <= 256 ? 8 : 16;   // rows per lane of the intra-task wavefront
   void* kintra = intra_tr == 8 ? (smem ? (void*)swk::k_intra16<8, true> : (void*)swk::k_intra16<8, false>)
@@ -1028,13 +1064,30 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   auto launch16 = [&](const uint2* words, const GroupDesc* groups, int n_groups_i, const int* n_groups_dev,
                       const int* pos_map, int n_long_r, int* counter_inter, int* counter_intra, int* score_out,
                       uint8_t* flag_out) -> int {
+    // only the first-pass layout has big slabs: elsewhere wide groups go intra-task
+    int cut_l = (n_groups_dev || variant == 1) ? std::min<int>(cut, (int)db->scratch_cols) : cut;
+    if (!n_groups_dev) {
+      const int64_t g0 = groups - db->d_groups;
+      const auto& gc = db->group_ncols;
+      n_long_r = (int)((gc.begin() + g0 + n_groups_i) - std::upper_bound(gc.begin() + g0, gc.begin() + g0 + n_groups_i, cut_l));
+    }
     const bool any_long = n_long_r > 0;
     long long scols = db->scratch_cols;
-    void* kargs_inter[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &cut,
+    // the range's inter-task groups wider than a warp slab: the first items of its queue
+    long long big_off = db->d_big ? (long long)(db->d_big - db->d_scratch) : 0;   // in uint2, same address space
+    int n_big_r = 0;
+    if (n_big && !n_groups_dev && variant != 1) {
+      const int64_t g0 = groups - db->d_groups, g1 = g0 + n_groups_i;
+      const auto& gc = db->group_ncols;
+      n_big_r = (int)(std::upper_bound(gc.begin() + g0, gc.begin() + g1, cut) -
+                      std::upper_bound(gc.begin() + g0, gc.begin() + g1, (int)db->scratch_cols));
+      n_big_r = std::max(0, n_big_r);
+    }
+    void* kargs_inter[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &cut_l,
                            &db->d_prof, (void*)&m_pad, (void*)&stride, &alpha, &beta, (void*)&limit16, &db->d_scratch,
-                           &scols, &counter_inter, &score_out, &flag_out};
+                           &scols, &counter_inter, &score_out, &flag_out, &big_off, &big_cols, &n_big_r};
     long long scols_intra = db->scratch_cols_intra;
-    void* kargs_intra[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &cut,
+    void* kargs_intra[] = {(void*)&words, (void*)&groups, &n_groups_i, (void*)&n_groups_dev, (void*)&pos_map, &cut_l,
                            &db->d_prof, (void*)&m_pad, (void*)&stride, &alpha, &beta, (void*)&limit16,
                            &db->d_scratch_intra, &scols_intra, &counter_intra, &score_out, &flag_out};
     cudaLaunchAttribute pdl[1];
@@ -1051,7 +1104,7 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
       const int grid_intra = (int)std::max<int64_t>(1, std::min<int64_t>(grid, (items + 11) / 12));
       if (kintra_qp && !n_groups_dev) {
         // f4 ablation: striped intra-task kernel (IntraQP) for the pair items
-        void* kargs_qp[] = {(void*)&words, (void*)&groups, &n_groups_i, &cut, &db->d_prof_qp, (void*)&qp_stride,
+        void* kargs_qp[] = {(void*)&words, (void*)&groups, &n_groups_i, &cut_l, &db->d_prof_qp, (void*)&qp_stride,
                             &alpha, &beta, (void*)&limit16, &counter_intra, &score_out, &flag_out};
         CK(cudaLaunchKernel(kintra_qp, dim3(grid_intra), dim3(swk::kInterThreads), kargs_qp, qp_bytes, st));
       } else {
@@ -1064,7 +1117,7 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
     cfg.gridDim = dim3(grid);
     if (variant == 1 && !n_groups_dev) {
       // f4 ablation: InterSP score profile instead of the query profile (SW_VARIANT=intersp)
-      void* kargs_sp[] = {(void*)&words, (void*)&groups, &n_groups_i, &cut, &db->d_query, (void*)&qlen,
+      void* kargs_sp[] = {(void*)&words, (void*)&groups, &n_groups_i, &cut_l, &db->d_query, (void*)&qlen,
                           (void*)&m_pad, &db->d_matrix, &alpha, &beta, (void*)&limit16, &db->d_scratch, &scols,
                           &counter_inter, &score_out, &flag_out};
       cfg.blockDim = dim3(swk::kInterThreads);

@@ -441,13 +441,14 @@ __device__ __forceinline__ int split_groups(const GroupDesc* __restrict__ groups
 }
 
 // Inter-task pass over groups [0, split): whole 64-subject groups, longest first.
-template <int T, bool SMEM, int NT>
+template <int T, bool SMEM, int NT, bool BIG = false>
 __global__ void __launch_bounds__(NT, 1)
 k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
           const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
-          int* __restrict__ score_sorted, uint8_t* __restrict__ flag) {
+          int* __restrict__ score_sorted, uint8_t* __restrict__ flag, long long big_off,
+          long long big_cols, int n_big) {
   extern __shared__ __align__(16) int8_t sprof[];
   __shared__ int s_split;
   if (n_groups_dev) n_groups = *n_groups_dev;   // mini-group layout of a rerun: size known on device only
@@ -460,7 +461,8 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   }
   if (SMEM) load_profile_smem(sprof, gprof, stride);
   const int lane = threadIdx.x & 31;
-  uint2* bnd = scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
+  const long long own = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
+  uint2* const own_bnd = scratch + own;
   const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
   for (;;) {
     int item = 0;
@@ -469,6 +471,11 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     if (item >= n_items) break;
     const int g = n_items - 1 - item;
     const GroupDesc gd = groups[g];
+    // the n_big longest groups (the first items) are wider than a warp's slab:
+    // each has a boundary slab of its own, big_off words from `scratch` (one
+    // base pointer keeps the slab accesses of the hot loop __restrict__)
+    uint2* bnd = own_bnd;
+    if constexpr (BIG) bnd = scratch + (item < n_big ? big_off + (long long)item * big_cols * 32 : own);
     const uint32_t hmax = inter_group16<T, SMEM>(words + gd.base, gd.ncols, gprof, stride, m_pad, bnd, na2, nb2, lane);
     emit_pair(hmax, g, 2 * lane, gd.count, limit, pos_map, score_sorted, flag);
   }
