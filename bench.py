@@ -183,6 +183,25 @@ def cpu_baseline(base, q, db, seconds_target=12.0):
             "sample": f"{n} random subjects of the rank-0 shard ({cells:.3e} cells, {dt:.1f} s)"}
 
 
+def traffic_model(lengths, m: int, n_warps: int = SMS * 12, tile_rows: int = 48) -> dict:
+    """Analytic DRAM bytes of one first pass: the packed database
+    (read once) plus the DP boundary rows that leave the registers -- 8 B per
+    lane-column written and read back at every internal query-tile edge of an
+    inter-task group, 8 B per pair-column per internal pass edge of an
+    intra-task pair.  (Boundary slabs exceed L2, so they go to HBM.)"""
+    ls = np.sort(np.asarray(lengths, dtype=np.int64))
+    ncols = ls[np.minimum(np.arange(0, ls.size, 64) + 63, ls.size - 1)]
+    m_pad = (m + 7) // 8 * 8
+    db_bytes = int(((ncols + 5) // 6 * 32 * 8).sum())
+    cut = max(128, int(ls.sum()) // (64 * n_warps))
+    inter, intra = ncols[ncols <= cut], ncols[ncols > cut]
+    tiles = -(-m_pad // tile_rows)
+    tr = 8 if m_pad <= 256 else 16
+    passes = -(-m_pad // (32 * tr))
+    bnd = int(inter.sum()) * 32 * 8 * 2 * (tiles - 1) + int(intra.sum()) * 32 * 8 * 2 * (passes - 1)
+    return {"db_bytes": db_bytes, "boundary_bytes": bnd, "total": db_bytes + bnd}
+
+
 def load_ncu_traffic():
     """DRAM bytes per k_inter16 launch from the newest committed ncu --set full summary."""
     import glob
@@ -333,7 +352,11 @@ def main():
                          "kernel": "k_inter16 (int16x2 DPX first pass)",
                          "kernel_ms": round(ms_inter, 4), "kernel_share_of_step": round(ms_inter / ms_step, 4),
                          "peak_basis": "148 SM x 1965 MHz x 64 DPX lanes/clk/SM (measured) / 1.75 alu-pipe ops per cell",
-                         **load_ncu_traffic()},
+                         **load_ncu_traffic(),
+                         "traffic_model": {**traffic_model(sdb.lengths, q.size),
+                                           "note": "analytic: packed DB read once + DP boundary rows at "
+                                                   "query-tile edges (DESIGN.md §5); the ncu traffic is "
+                                                   "this, not re-reads of the input"}},
             "clocks": clk,
             "gpu_launches": int(launches),
             "e2e": e2e,
