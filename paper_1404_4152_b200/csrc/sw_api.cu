@@ -978,8 +978,9 @@ static int search_enqueue(sw_db* db, const uint8_t* query, int32_t qlen, const i
   long long big_cols = 0;
   int n_big = 0;
   {
-    constexpr int64_t kMaxBig = 2048;
+    int64_t kMaxBig = 2048;
     constexpr int64_t kBigBytes = 8LL << 30;
+    if (const char* e = getenv("SW_MAX_BIG")) kMaxBig = std::max<int64_t>(0, atoll(e));   // tests: the fallback
     const auto& gc = db->group_ncols;
     const int64_t b0 = std::upper_bound(gc.begin(), gc.end(), (int)db->scratch_cols) - gc.begin();
     int64_t b1 = std::upper_bound(gc.begin(), gc.end(), cut) - gc.begin();   // inter-task groups: [0, b1)

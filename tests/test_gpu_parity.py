@@ -313,8 +313,9 @@ def test_persistent_index_roundtrip(tmp_path):
 
 @pytest.mark.parametrize("first_stage", [16, 8, 32])
 def test_very_long_subjects_exceeding_boundary_slab(first_stage):
-    """Subjects longer than the per-warp boundary slab (6,144 columns) are always
-    aligned intra-task (or rerun), in every stage; scores stay exact."""
+    """Subjects longer than the per-warp boundary slab (6,144 columns): inter-task
+    with slabs of their own (first pass), intra-task or rerun elsewhere, in every
+    stage; scores stay exact."""
     rng = np.random.default_rng(91)
     lens = np.concatenate([rng.integers(1, 300, size=200), [7000, 9000, 20000, 6145, 6144]])
     db = random_db(91, lens)
@@ -325,3 +326,27 @@ def test_very_long_subjects_exceeding_boundary_slab(first_stage):
         r = g.search_batch([q, _query(300, 92)], B62, 2, 12, k=5)
     for i, qq in enumerate([q, _query(300, 92)]):
         assert np.array_equal(r.scores[i], oracle.db_scores(qq, db, B62, 2, 12))
+
+
+@pytest.mark.parametrize("max_big", ["0", "2", "1000"])
+def test_wide_groups_big_slabs_and_fallback(monkeypatch, max_big):
+    """Groups wider than a warp's slab take per-item slabs (the first items of the
+    longest-first queue); with SW_MAX_BIG below their number the widest fall back
+    to the intra-task wavefront.  Every split gives the oracle's scores."""
+    monkeypatch.setenv("SW_MAX_BIG", max_big)
+    rng = np.random.default_rng(77)
+    lens = np.concatenate([rng.integers(1, 400, size=600), rng.integers(6200, 9000, size=320)])
+    db = random_db(77, lens)
+    q = _query(150, 77)
+    for t in (600, 700, 919):                                  # strong hits inside wide subjects
+        db.residues[db.offsets[t] + 3000:db.offsets[t] + 3150] = q
+    _check(db, q, B62, 2, 12, k=8, long_threshold=-1)
+
+
+def test_empty_database():
+    empty = random_db(3, np.zeros(0, dtype=np.int64))
+    with sw.Database(empty.residues, empty.offsets, empty.lengths, device=0) as g:
+        r = g.search(_query(50, 3), B62, 2, 12, k=4)
+        assert r.scores.size == 0
+        assert r.topk_ids.tolist() == [-1] * 4 and r.topk_scores.tolist() == [-1] * 4
+        assert g.align(_query(50, 3), B62, 2, 12, []) == []
