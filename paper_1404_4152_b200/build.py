@@ -10,9 +10,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread",
            "-diag-suppress", "550"]
 SOURCES = [os.path.join(PKG, "csrc", "sw_api.cu")]
-DEPS = SOURCES + [os.path.join(PKG, "csrc", "sw_kernels.cuh"), os.path.join(PKG, "csrc", "sw_align.cuh"),
-                  os.path.join(PKG, "csrc", "sw_ablation.cuh"),
-                  os.path.join(ROOT, "include", "swsearch.h")]
+DEPS = SOURCES + [os.path.join(PKG, "csrc", f) for f in sorted(os.listdir(os.path.join(PKG, "csrc")))
+                  if f.endswith((".cuh", ".inc"))] + [os.path.join(ROOT, "include", "swsearch.h")]
 OUT = os.path.join(PKG, "libswsearch.so")
 
 
