@@ -151,6 +151,7 @@ struct sw_db {
 
   uint2* d_scratch = nullptr;     // DP boundary rows, one slab per resident warp (inter-task kernels)
   uint2* d_scratch_intra = nullptr; // pass boundaries of the intra-task kernel (runs concurrently: own slabs)
+  uint2* d_scratch_intra2 = nullptr; // f1: the second query's intra-task pass (allocated on first use)
   long long scratch_cols_intra = 0;
   long long scratch_cols = 0;
   int scratch_slots = 0;

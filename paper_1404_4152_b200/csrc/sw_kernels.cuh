@@ -505,7 +505,10 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   __syncthreads();
   const int split = s_split;
   const int n_items = (n_groups - split) * 32;
-  if (n_items <= 0) return;
+  if (n_items <= 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   if (SMEM) load_profile_smem(sprof, gprof, stride);
   const int lane = threadIdx.x & 31;
   uint2* bnd = scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
@@ -525,6 +528,9 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     for (int o = 16; o > 0; o >>= 1) hm = __vmaxs2(hm, __shfl_xor_sync(0xffffffffu, hm, o));
     if (lane == 0) emit_pair(hm, g, 2 * p, gd.count, limit, pos_map, score_sorted, flag);
   }
+  // When launched as a programmatic dependent (a chain of intra-task passes in
+  // sw_search_batch), retire only after the primary grid: a no-op otherwise.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -1020,17 +1026,20 @@ __global__ void k_profile_pair(const uint8_t* __restrict__ qa, int ma, const uin
 // Items: half-groups (32 subjects, the lo or hi members of a 64-subject group), longest first.
 template <int T>
 __global__ void __launch_bounds__(kInterThreads, 1)
-k_multi16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
+k_multi16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups, int cut,
           const uint32_t* __restrict__ gprof2, int m_pad, int stride2, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
           int* __restrict__ score_a, int* __restrict__ score_b, uint8_t* __restrict__ flag_a,
           uint8_t* __restrict__ flag_b) {
   extern __shared__ __align__(16) uint32_t sprof2[];
+  __shared__ int s_split;
   {
+    if (threadIdx.x == 0) s_split = split_groups(groups, n_groups, cut);   // wider groups: k_intra16 per query
     const int n4 = kProfRows * stride2;
     for (int t = threadIdx.x; t < n4; t += blockDim.x) sprof2[t] = __ldg(gprof2 + t);
     __syncthreads();
   }
+  n_groups = s_split;
   const int lane = threadIdx.x & 31;
   const long long wslot = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   uint2* bnd = scratch + wslot * scratch_cols * 32;
@@ -1069,6 +1078,7 @@ k_multi16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
       if (b > limit || b < 0) flag_b[pos] = 1;
     }
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // programmatic dependent of the intra-task passes
 }
 
 // ---------------------------------------------------------------------------

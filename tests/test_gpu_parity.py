@@ -252,15 +252,18 @@ def test_search_validation_errors():
         assert ei.value.code == sw.SW_ERANGE
 
 
-def test_batched_queries_equal_single_searches():
+@pytest.mark.parametrize("long_threshold", [0, 64, -1])
+def test_batched_queries_equal_single_searches(long_threshold):
     """f1: queries paired in one int16x2 pass give exactly the per-query oracle
-    scores and top-k (odd count, unequal lengths, one query too long to pair)."""
+    scores and top-k (odd count, unequal lengths, lengths too far apart to pair,
+    one query too long to pair).  long_threshold 64 sends most groups pair by
+    pair through the two intra-task passes that run beside the joint pass."""
     rng = np.random.default_rng(77)
     db = random_db(77, np.concatenate([rng.integers(0, 900, size=1500), [0, 1, 5000]]))
-    qs = [_query(m, 30 + i) for i, m in enumerate([1, 100, 333, 464, 47, 2600, 129])]
-    with sw.Database.from_synth(db, device=0) as g:
+    qs = [_query(m, 30 + i) for i, m in enumerate([1, 100, 333, 464, 420, 47, 2600, 129, 120])]
+    with sw.Database.from_synth(db, device=0, long_threshold=long_threshold) as g:
         r = g.search_batch(qs, B62, 2, 12, k=12)
-    assert r.stats["pairs"] == 3
+    assert r.stats["pairs"] == 2                       # (464, 420) and (129, 120): min/max >= 0.85
     for i, q in enumerate(qs):
         ref = oracle.db_scores(q, db, B62, 2, 12)
         assert np.array_equal(r.scores[i], ref), i
