@@ -219,6 +219,14 @@ int sw_align(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix
              int32_t beta, const int64_t* subjects, int32_t n, sw_alignment* out, char* ops, int64_t ops_cap);
 
 /*
+ * Letters -> residue codes (host helper): the 24-letter table
+ * "ARNDCQEGHILKMFPSTWYVBZX*" -> 0..23, case-insensitive; letters outside it
+ * (J, O, U) -> 22 ('X').  Any other byte -> SW_EINVAL naming its position;
+ * `out` (n bytes) is left untouched on error.
+ */
+int sw_encode(const char* text, int64_t n, uint8_t* out);
+
+/*
  * Merge n_lists top-k lists (host; e.g. one per GPU after an all-gather) into
  * the global top-k by (score desc, id asc).  Entries with id < 0 are ignored.
  *   ids/scores   host, n_lists * k_in entries (list-major)

@@ -65,7 +65,7 @@ class sw_alignment(ctypes.Structure):
 
 # Every symbol include/swsearch.h declares (tests check the .so exports all of them).
 EXPORTS = ("sw_opts_default", "sw_db_create", "sw_search", "sw_search_async", "sw_search_batch", "sw_merge_topk",
-           "sw_db_get_info", "sw_db_stage_times", "sw_align", "sw_db_save", "sw_db_load", "sw_db_destroy", "sw_strerror",
+           "sw_db_get_info", "sw_db_stage_times", "sw_align", "sw_encode", "sw_db_save", "sw_db_load", "sw_db_destroy", "sw_strerror",
            "sw_last_error")
 
 _lib = None
@@ -91,6 +91,8 @@ def lib() -> ctypes.CDLL:
         L.sw_search_batch.restype = ctypes.c_int
         L.sw_align.argtypes = [P, P, i32, P, i32, i32, P, i32, ctypes.POINTER(sw_alignment), P, i64]
         L.sw_align.restype = ctypes.c_int
+        L.sw_encode.argtypes = [ctypes.c_char_p, i64, P]
+        L.sw_encode.restype = ctypes.c_int
         L.sw_merge_topk.argtypes = [P, P, i32, i32, i32, P, P]
         L.sw_merge_topk.restype = ctypes.c_int
         L.sw_db_get_info.argtypes = [P, ctypes.POINTER(sw_db_info)]
@@ -290,6 +292,14 @@ class Database:
 
     def __exit__(self, *a):
         self.close()
+
+
+def encode(text) -> np.ndarray:
+    """sw_encode: protein letters (str or bytes) -> residue codes uint8 (J, O, U -> X)."""
+    raw = text.encode("ascii") if isinstance(text, str) else bytes(text)
+    out = np.empty(len(raw), dtype=np.uint8)
+    _check(lib().sw_encode(raw, len(raw), out.ctypes.data if out.size else None))
+    return out
 
 
 def merge_topk(ids: np.ndarray, scores: np.ndarray, k_out: int):

@@ -215,6 +215,24 @@ extern "C" {
 #include "sw_batch.inc"
 #include "sw_align_host.inc"
 
+int sw_encode(const char* text, int64_t n, uint8_t* out) {
+  if (n < 0 || (n > 0 && (!text || !out))) return fail(SW_EINVAL, "sw_encode: bad arguments");
+  static const char kAlphabet[] = "ARNDCQEGHILKMFPSTWYVBZX*";
+  uint8_t lut[256];
+  memset(lut, 255, sizeof lut);
+  for (int c = 'A'; c <= 'Z'; c++) lut[c] = lut[c + 32] = 22;   // letters outside the table -> X
+  for (int i = 0; i < 24; i++) {
+    const unsigned char c = (unsigned char)kAlphabet[i];
+    lut[c] = (uint8_t)i;
+    if (c >= 'A' && c <= 'Z') lut[c + 32] = (uint8_t)i;
+  }
+  for (int64_t i = 0; i < n; i++)
+    if (lut[(unsigned char)text[i]] == 255)
+      return fail(SW_EINVAL, "sw_encode: invalid residue byte 0x%02x at position %lld", (unsigned char)text[i], (long long)i);
+  for (int64_t i = 0; i < n; i++) out[i] = lut[(unsigned char)text[i]];
+  return SW_OK;
+}
+
 // Host merge of per-device top-k lists (the multi-GPU exchange step, DESIGN.md §"Multi-GPU").
 int sw_merge_topk(const int64_t* ids, const int32_t* scores, int32_t n_lists, int32_t k_in, int32_t k_out,
                   int64_t* out_ids, int32_t* out_scores) {

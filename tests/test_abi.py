@@ -99,3 +99,16 @@ def test_db_load_rejects_bad_files(tmp_path, content):
     with pytest.raises(sw.SwError) as ei:
         sw.Database.load(str(path))
     assert ei.value.code == sw.SW_EINVAL
+
+
+def test_encode_matches_alphabet_table():
+    from swdata import encode as ref_encode
+    rng = np.random.default_rng(5)
+    letters = "ARNDCQEGHILKMFPSTWYVBZX*JOUarndcqeghilkmfpstwyvbzxjou"
+    for n in (0, 1, 7, 1000):
+        text = "".join(rng.choice(list(letters), size=n))
+        assert np.array_equal(sw.encode(text), ref_encode(text)), text[:20]
+    assert sw.encode("ARNDJ*").tolist() == [0, 1, 2, 3, 22, 23]
+    with pytest.raises(sw.SwError) as e:
+        sw.encode("AR1N")
+    assert e.value.code == sw.SW_EINVAL and b"position 2" in sw.lib().sw_last_error()
