@@ -15,13 +15,14 @@
 // every decision is the one the oracle's full-matrix traceback takes.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace swk {
 
 struct AlignJob {
   long long word0;   // first packed word (uint2 units) of the subject's group + its lane
-  long long dir;     // direction words of this job (uint32 units): (m_pad/TR) x n
+  long long dir;     // direction words of this job (DirWord<TR> units): (m_pad/TR) x n
   long long bnd;     // pass boundary (H, E) of this job (int2 units): 2 x n
   long long ops;     // first byte of this job's ops slot (capacity m + n)
   long long tmp;     // first byte of its reversed-ops scratch (capacity m + n)
@@ -53,7 +54,10 @@ __device__ __forceinline__ bool better(int h, int j, int i, int bh, int bj, int 
   return h > bh || (h == bh && (j < bj || (j == bj && i < bi)));
 }
 
-constexpr int kAlignWarps = 8;       // warps per hit: one 32*TR-row band each, pipelined along the columns
+// warps per hit: one 32*TR-row band each, pipelined along the columns (256 / TR x 32 = 1,024 rows per round)
+template <int TR> constexpr int align_warps() { return 64 / TR; }
+// direction word of one lane-row-block and column: TR 4-bit codes
+template <int TR> using DirWord = typename std::conditional<TR == 8, uint32_t, uint16_t>::type;
 constexpr int kRing = 128;           // columns of (H, E) in flight between neighbouring warps (shared memory)
 
 // res[t*6 + ...] = score, q_begin, q_end, s_begin, s_end, n_ops
@@ -63,11 +67,11 @@ constexpr int kRing = 128;           // columns of (H, E) in flight between neig
 // lane wavefront, taking the row above its band from warp w-1 through a
 // shared-memory ring (or, for warp 0, from the previous round's last warp
 // through global memory) and running ~64 columns behind it.
-template <int TR>
+template <int TR, int kAlignWarps = align_warps<TR>()>
 __global__ void __launch_bounds__(32 * kAlignWarps)
 k_align(const uint2* __restrict__ words, const AlignJob* __restrict__ jobs, int n_jobs,
         const int8_t* __restrict__ prof, int prof_smem, int stride, int m, int m_pad, int alpha, int beta,
-        uint32_t* __restrict__ dir, int2* __restrict__ bnd, char* __restrict__ ops_out,
+        DirWord<TR>* __restrict__ dir, int2* __restrict__ bnd, char* __restrict__ ops_out,
         char* __restrict__ ops_tmp, int* __restrict__ res) {
   const int t = blockIdx.x;
   if (t >= n_jobs) return;
@@ -75,7 +79,7 @@ k_align(const uint2* __restrict__ words, const AlignJob* __restrict__ jobs, int 
   const AlignJob J = jobs[t];
   const int n = J.n;
   const uint32_t* wp = reinterpret_cast<const uint32_t*>(words + J.word0) + J.half;   // word w at wp[64 w]
-  uint32_t* D = dir + J.dir;
+  DirWord<TR>* D = dir + J.dir;
   int2* B = bnd + J.bnd;
   int best = 0, bj = 0x7fffffff, bi = 0x7fffffff;
   int stalled = 0;
@@ -157,29 +161,49 @@ k_align(const uint2* __restrict__ words, const AlignJob* __restrict__ jobs, int 
             cc = c0;
           }
           if (lane < nact && j >= 0 && j < n) {
-            const uint2 pv = *reinterpret_cast<const uint2*>(pr + cc * stride);
-            int hu = h_in, eu = e_in, dg = hdiag;
+            uint2 pv;
+            if constexpr (TR == 8) pv = *reinterpret_cast<const uint2*>(pr + cc * stride);
+            else pv = make_uint2(*reinterpret_cast<const uint32_t*>(pr + cc * stride), 0u);
+            // E(i+1,j) = max(E(i,j) - alpha, H(i,j) - beta) = max(E(i,j) - alpha, Y(i,j) - beta)
+            // with Y = max(0, G, F): since alpha <= beta the E - beta term never wins, so the
+            // E chain from row to row is one max; H, the direction code and the
+            // running max hang off it.  Extension bit of E(i+1,j):
+            // E - alpha > H - beta  <=>  alpha < beta  and  E - alpha > Y - beta.
+            int dg = hdiag;
+            int ec = max(e_in - alpha, h_in - beta);                 // E(i0, j)
+            uint32_t ecx = e_in - alpha > h_in - beta ? 4u : 0u;      // its extension bit
             uint32_t nib = 0;
+            int eu = 0;
+            int cm = 0;                                              // column max over real rows
 #pragma unroll
             for (int r = 0; r < TR; r++) {
               const int sub = (int)(int8_t)(((r < 4 ? pv.x : pv.y) >> (8 * (r & 3))) & 0xffu);
-              const int G = dg + sub;                              // H(i-1,j-1) + fsbt(q_i, s_j)
-              const int eo = hu - beta, ee = eu - alpha;
-              const int E = max(ee, eo);                           // E(i,j)
+              const int G = dg + sub;                                // H(i-1,j-1) + fsbt(q_i, s_j)
               const int fo = Hc[r] - beta, fe = Fc[r] - alpha;
-              const int F = max(fe, fo);                           // F(i,j)
-              const int H = max(max(0, G), max(E, F));
-              const uint32_t src = H == 0 ? 0u : H == G ? 1u : H == E ? 2u : 3u;
-              nib |= (src | (ee > eo ? 4u : 0u) | (fe > fo ? 8u : 0u)) << (4 * r);
-              const int i = i0 + r;
-              if (i < m && better(H, j, i, best, bj, bi)) { best = H; bj = j; bi = i; }
-              dg = Hc[r];                                          // H(i, j-1): diagonal of row i+1
+              const int F = max(fe, fo);                             // F(i,j)
+              const int Y = max(max(G, F), 0);
+              const int H = max(Y, ec);                              // H(i,j)
+              const uint32_t src = H == 0 ? 0u : H == G ? 1u : H == ec ? 2u : 3u;
+              nib |= (src | ecx | (fe > fo ? 8u : 0u)) << (4 * r);
+              if (r == TR - 1) eu = ec;                              // E of the lane's last row
+              const int yb = Y - beta, ee = ec - alpha;
+              ecx = (alpha < beta && ee > yb) ? 4u : 0u;
+              ec = max(ee, yb);                                      // E(i+1,j)
+              cm = max(cm, i0 + r < m ? H : 0);
+              dg = Hc[r];                                            // H(i, j-1): diagonal of row i+1
               Hc[r] = H;
               Fc[r] = F;
-              hu = H;
-              eu = E;
             }
-            D[(long long)(i0 / TR) * n + j] = nib;
+            if (cm > 0 && cm >= best) {                              // rare: locate the first row reaching it
+#pragma unroll
+              for (int r = 0; r < TR; r++)
+                if (i0 + r < m && Hc[r] == cm) {
+                  if (better(cm, j, i0 + r, best, bj, bi)) { best = cm; bj = j; bi = i0 + r; }
+                  break;
+                }
+            }
+            const int hu = Hc[TR - 1];                               // (H, E) of the last row for the next lane
+            D[(long long)(i0 / TR) * n + j] = (DirWord<TR>)nib;
             if (lane == nact - 1 && !last) {
               if (to_ring) ring[warp][j % kRing] = make_int2(hu, eu);
               else gout[j] = make_int2(hu, eu);
@@ -236,7 +260,7 @@ k_align(const uint2* __restrict__ words, const AlignJob* __restrict__ jobs, int 
         wrb = rb;
         wcj = j;
         const int lr = wrb - (lane >> 4), lc = wcj - 15 + (lane & 15);
-        win = (lr >= 0 && lc >= 0) ? __ldcg(D + (long long)lr * n + lc) : 0u;
+        win = (lr >= 0 && lc >= 0) ? (uint32_t)__ldcg(D + (long long)lr * n + lc) : 0u;
       }
       const uint32_t w = __shfl_sync(0xffffffffu, win, 16 * (wrb - rb) + (j - (wcj - 15)));
       const uint32_t nib = (w >> (4 * (i % TR))) & 15u;
