@@ -1315,6 +1315,84 @@ __global__ void __launch_bounds__(1024) k_topk_small(const unsigned long long* _
   }
 }
 
+// Small databases (n <= 65,536, min(k, n) <= 4,096): the whole ranking in ONE
+// CTA -- radix select of the k-th largest unique key (8 bits per pass, smem
+// histogram), compaction of the k keys above it, bitonic sort, decode --
+// instead of the 19-launch multi-CTA path.
+__global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* __restrict__ keys, int n, int k,
+                                                     long long* __restrict__ out_ids, int* __restrict__ out_scores) {
+  __shared__ unsigned long long s[4096];
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long sh_prefix, sh_mask;
+  __shared__ long long sh_kk;
+  __shared__ int sh_cnt;
+  const int cnt = min(k, n);
+  unsigned long long thr = 0ull;
+  if (k < n) {
+    if (threadIdx.x == 0) { sh_prefix = 0ull; sh_mask = 0ull; sh_kk = k; }
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0u;
+      __syncthreads();
+      const unsigned long long prefix = sh_prefix, mask = sh_mask;
+      for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        const unsigned long long key = keys[p];
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {                                  // digit with (# > d) < kk <= (# >= d)
+        long long above = 0;
+        const long long kk = sh_kk;
+        for (int d = 255; d >= 0; d--) {
+          const long long c = hist[d];
+          if (above < kk && kk <= above + c) {
+            sh_kk = kk - above;
+            sh_prefix = prefix | ((unsigned long long)d << shift);
+            sh_mask = mask | (255ull << shift);
+            break;
+          }
+          above += c;
+        }
+      }
+      __syncthreads();
+    }
+    thr = sh_prefix;                                           // the k-th largest key (keys are unique)
+  }
+  if (threadIdx.x == 0) sh_cnt = 0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    const unsigned long long key = keys[p];
+    if (key >= thr) s[atomicAdd(&sh_cnt, 1)] = key;
+  }
+  __syncthreads();
+  int n2 = 1;
+  while (n2 < cnt) n2 <<= 1;
+  for (int t = cnt + threadIdx.x; t < n2; t += blockDim.x) s[t] = 0ull;
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+        const int u = t ^ stride;
+        if (u > t) {
+          const bool desc = (t & size) == 0;
+          const unsigned long long a = s[t], b = s[u];
+          if (desc ? (a < b) : (a > b)) { s[t] = b; s[u] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    if (t < cnt) {
+      const unsigned long long key = s[t];
+      if (out_ids) out_ids[t] = (long long)(0xffffffffull - (key & 0xffffffffull));
+      if (out_scores) out_scores[t] = (int)(key >> 32);
+    } else {
+      if (out_ids) out_ids[t] = -1;
+      if (out_scores) out_scores[t] = -1;
+    }
+  }
+}
+
 __global__ void k_topk_decode(const unsigned long long* __restrict__ sorted, int cnt, int k,
                               long long* __restrict__ out_ids, int* __restrict__ out_scores) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < k; t += gridDim.x * blockDim.x) {
