@@ -83,6 +83,11 @@ void* inter16_kernel(bool smem, bool big) {
   if (big) return smem ? (void*)swk::k_inter16<T, true, NT, true> : (void*)swk::k_inter16<T, false, NT, true>;
   return smem ? (void*)swk::k_inter16<T, true, NT> : (void*)swk::k_inter16<T, false, NT>;
 }
+// f4 ablation (SW_VARIANT=static): the paper's static loop schedule instead of the work queue
+inline void* inter16_kernel_static(bool smem, bool big) {
+  if (big) return smem ? (void*)swk::k_inter16<48, true, 384, true, true> : (void*)swk::k_inter16<48, false, 384, true, true>;
+  return smem ? (void*)swk::k_inter16<48, true, 384, false, true> : (void*)swk::k_inter16<48, false, 384, false, true>;
+}
 
 template <int T>
 void* inter16_kernel_nt(bool smem, int nt, bool big) {

@@ -441,7 +441,7 @@ __device__ __forceinline__ int split_groups(const GroupDesc* __restrict__ groups
 }
 
 // Inter-task pass over groups [0, split): whole 64-subject groups, longest first.
-template <int T, bool SMEM, int NT, bool BIG = false>
+template <int T, bool SMEM, int NT, bool BIG = false, bool STATIC = false>
 __global__ void __launch_bounds__(NT, 1)
 k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
           const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
@@ -464,10 +464,16 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   const long long own = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
   uint2* const own_bnd = scratch + own;
   const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
+  int it_static = 0;
   for (;;) {
     int item = 0;
-    if (lane == 0) item = atomicAdd(counter, 1);
-    item = __shfl_sync(0xffffffffu, item, 0);
+    if constexpr (STATIC) {
+      // f4 ablation of the paper's OpenMP "static" schedule: item w + t*W
+      item = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) + it_static++ * gridDim.x * (blockDim.x >> 5);
+    } else {
+      if (lane == 0) item = atomicAdd(counter, 1);
+      item = __shfl_sync(0xffffffffu, item, 0);
+    }
     if (item >= n_items) break;
     const int g = n_items - 1 - item;
     const GroupDesc gd = groups[g];

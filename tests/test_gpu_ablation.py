@@ -18,7 +18,7 @@ def _query(m, seed=0):
     return gen_residues(stream_key(seed, "ablation-query", m), 0, m)
 
 
-@pytest.mark.parametrize("variant", ["intersp", "intraqp"])
+@pytest.mark.parametrize("variant", ["intersp", "intraqp", "static"])
 @pytest.mark.parametrize("m", [1, 8, 31, 33, 100, 464, 1100])
 def test_variant_equals_oracle(monkeypatch, variant, m):
     monkeypatch.setenv("SW_VARIANT", variant)

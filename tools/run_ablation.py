@@ -24,7 +24,7 @@ print(json.dumps({"ms_first_pass": round(t, 3), "gcups_first_pass": round(cells 
 ''' % ROOT
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="C2,C4")
-ap.add_argument("--variants", default="base,intersp,intra,intraqp")
+ap.add_argument("--variants", default="base,intersp,intra,intraqp,static")
 ap.add_argument("--json", default=None)
 a = ap.parse_args()
 rows = []
@@ -33,7 +33,7 @@ for cfgname in a.configs.split(","):
         env = dict(os.environ)
         env.pop("SW_VARIANT", None)
         env.pop("SW_LONG_COLS", None)
-        if v in ("intersp", "intraqp"):
+        if v in ("intersp", "intraqp", "static"):
             env["SW_VARIANT"] = v
         if v in ("intra", "intraqp"):                    # every group through the intra-task path
             env["SW_LONG_COLS"] = "1"
