@@ -349,6 +349,9 @@ def main():
             "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_max, 1),
                          "unit": "Gcell/s", "frac": round(achieved / peak_max, 4),
                          "frac_at_run_clock": round(achieved / peak_run, 4),
+                         # one PRMT per int16x2 row merges the two subjects' substitution scores
+                         # (2.25 alu ops per cell): the kernel's own instruction-mix bound
+                         "frac_of_mix_bound_2p25": round(achieved / (peak_max * ALU_OPS_PER_CELL / 2.25), 4),
                          "kernel": "k_inter16 (int16x2 DPX first pass)",
                          "kernel_ms": round(ms_inter, 4), "kernel_share_of_step": round(ms_inter / ms_step, 4),
                          "peak_basis": "148 SM x 1965 MHz x 64 DPX lanes/clk/SM (measured) / 1.75 alu-pipe ops per cell",
