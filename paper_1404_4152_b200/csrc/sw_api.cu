@@ -95,6 +95,34 @@ void* inter16_kernel_nt(bool smem, int nt, bool big) {
 }
 constexpr int kMaxSmemProfile = 200 * 1024;
 
+// Shape of the intra-task wavefront's blocked profile: TR rows per lane, the
+// fewest that put the query in one 32-lane pass (TR in {4, 6, 8, 12, 16}; longer
+// queries take several passes of 16 rows per lane), so few lanes idle.
+struct IntraShape {
+  int tr, nblk, rowstride;
+  size_t bytes;
+  bool smem;
+};
+IntraShape intra_shape(int m_pad) {
+  const int need = (m_pad + 31) / 32;
+  IntraShape sh;
+  sh.tr = need <= 4 ? 4 : need <= 6 ? 6 : need <= 8 ? 8 : need <= 12 ? 12 : 16;
+  sh.nblk = (m_pad + sh.tr - 1) / sh.tr;
+  sh.rowstride = sh.nblk * 16;
+  sh.bytes = (size_t)swk::kProfRows * sh.rowstride;
+  sh.smem = sh.bytes <= (size_t)kMaxSmemProfile;
+  return sh;
+}
+void* intra_kernel(const IntraShape& sh) {
+  switch (sh.tr) {
+    case 4: return sh.smem ? (void*)swk::k_intra16<4, true> : (void*)swk::k_intra16<4, false>;
+    case 6: return sh.smem ? (void*)swk::k_intra16<6, true> : (void*)swk::k_intra16<6, false>;
+    case 8: return sh.smem ? (void*)swk::k_intra16<8, true> : (void*)swk::k_intra16<8, false>;
+    case 12: return sh.smem ? (void*)swk::k_intra16<12, true> : (void*)swk::k_intra16<12, false>;
+    default: return sh.smem ? (void*)swk::k_intra16<16, true> : (void*)swk::k_intra16<16, false>;
+  }
+}
+
 int host_threads() {
   unsigned n = std::thread::hardware_concurrency();
   return (int)std::max(1u, std::min(n, 64u));
@@ -149,6 +177,9 @@ struct sw_db {
   int* d_inv = nullptr;           // input index -> sorted position (built on the first sw_align)
   uint2* d_big = nullptr;         // boundary slabs of the inter-task groups wider than a warp's slab
   size_t big_cap = 0;
+  int8_t* d_profb = nullptr;      // blocked profile of the intra-task wavefront (and f1's second query)
+  int8_t* d_profb2 = nullptr;
+  size_t profb_cap = 0, profb2_cap = 0;
   int8_t* d_prof_qp = nullptr;    // f4 IntraQP ablation: profile with rows of 32*L bytes
   size_t prof_qp_cap = 0;
   void* aw[10] = {};              // sw_align workspace (grow-only): idx, jobs, res, q, M, prof, dir, bnd, ops, tmp

@@ -72,6 +72,20 @@ __device__ __forceinline__ uint32_t pack2(int v) {
 // profile holds fsbt(q_i, r) for every query position i; int8, one row per
 // residue code, DUMMY row and padded query positions are 0.
 // ---------------------------------------------------------------------------
+// Blocked profile of the intra-task wavefront: residue row r holds nblk blocks
+// of 16 bytes; block b = fsbt(q_i, r) for query rows i = b*TR .. b*TR+TR-1
+// (0 past the query and in the unused bytes).  Row stride = nblk * 16 bytes.
+__global__ void k_profile_blk(const uint8_t* __restrict__ q, int m, const int8_t* __restrict__ M,
+                              int8_t* __restrict__ profb, int tr, int nblk) {
+  const int row = nblk * 16, total = kProfRows * row;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int r = t / row, rem = t - r * row, b = rem >> 4, k = rem & 15, i = b * tr + k;
+    int8_t v = 0;
+    if (k < tr && i < m && r < kNumCodes) v = M[q[i] * 32 + r];
+    profb[t] = v;
+  }
+}
+
 __global__ void k_profile(const uint8_t* __restrict__ q, int m, const int8_t* __restrict__ M,
                           int8_t* __restrict__ prof, int stride) {
   const int total = kProfRows * stride;
@@ -126,6 +140,33 @@ __device__ __forceinline__ uint32_t col16(uint32_t (&D)[R], uint32_t (&F)[R], ui
     a = an;
     b = bn;
   }
+  return hprev;
+}
+
+// Column of R <= 16 rows whose profile bytes for the lane (lo and hi subject)
+// are one 16-byte block each (the intra-task "blocked" profile: block b holds
+// query rows [b*R, b*R + R), zero-padded).  Same cell update as col16.
+template <int R>
+__device__ __forceinline__ uint32_t col16b(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t& e, uint32_t htop,
+                                           const uint4 a, const uint4 b, uint32_t na2, uint32_t nb2,
+                                           uint32_t& hmax) {
+  static_assert(R >= 2 && R <= 16, "blocked profile rows");
+  uint32_t hprev = htop, hodd = 0u;
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    const uint32_t wa = r < 4 ? a.x : r < 8 ? a.y : r < 12 ? a.z : a.w;
+    const uint32_t wb = r < 4 ? b.x : r < 8 ? b.y : r < 12 ? b.z : b.w;
+    const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);
+    const uint32_t sn = prmt(wa, wb, sel_pair(r & 3));
+    D[r] = __vadd2(hprev, sn);
+    const uint32_t hb = __vadd2(h, nb2);
+    e = __viaddmax_s16x2_relu(e, na2, hb);
+    F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+    if (r & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
+    else hodd = h;
+    hprev = h;
+  }
+  if (R & 1) hmax = __vmaxs2(hmax, hodd);
   return hprev;
 }
 
@@ -333,7 +374,7 @@ __device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, i
     const bool first = base == 0, last = base + 32 * TR >= m_pad;
     const uint2* gin = gbnd + (long long)(pass & 1) * gstride;          // written by the previous pass
     uint2* gout = gbnd + (long long)((pass + 1) & 1) * gstride;
-    const int8_t* pr = prof + base + lane * TR;
+    const int8_t* pr = prof + (base / TR + lane) * 16;                 // this lane's 16-byte profile block
     uint32_t D[TR], F[TR];
 #pragma unroll
     for (int r = 0; r < TR; r++) { D[r] = 0u; F[r] = 0u; }
@@ -375,8 +416,9 @@ __device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, i
         }
         if (lane < nact && j >= -1 && j < ncols) {
           uint32_t e = e_in;
-          const uint32_t hl = col16<TR>(D, F, e, h_in, pr + (r_in & 31u) * stride, pr + (r_in >> 5) * stride,
-                                        na2, nb2, hmax);
+          const uint4 pa = *reinterpret_cast<const uint4*>(pr + (r_in & 31u) * stride);
+          const uint4 pb = *reinterpret_cast<const uint4*>(pr + (r_in >> 5) * stride);
+          const uint32_t hl = col16b<TR>(D, F, e, h_in, pa, pb, na2, nb2, hmax);
           e_out = e;
           h_out = hl;
           r_out = r_in;
