@@ -13,7 +13,8 @@
 // then includes the ABI in parts -- sw_db.inc (create / save / load / info),
 // sw_search.inc (sw_search, sw_search_async, streamed databases),
 // sw_batch.inc (f1), sw_align_host.inc (f3) -- and ends with sw_merge_topk.
-// Device code: sw_kernels.cuh (search), sw_align.cuh (f3), sw_ablation.cuh (f4).
+// Device code: sw_kernels.cuh (search: sw_common / sw_int16 / sw_int8 / sw_int32
+// / sw_multi / sw_escalate / sw_rank .cuh), sw_align.cuh (f3), sw_ablation.cuh (f4).
 #include <cuda_runtime.h>
 
 #include <algorithm>

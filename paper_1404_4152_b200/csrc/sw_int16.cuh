@@ -1,0 +1,413 @@
+// sw_int16.cuh -- the int16x2 DPX first pass: cell update, register tiles, inter-task and intra-task kernels (a3, a5)
+// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+#pragma once
+#include "sw_common.cuh"
+
+namespace swk {
+
+// ---------------------------------------------------------------------------
+// One column j of R query rows [i0, i0+R) for a pair of subjects (int16x2).
+//   in : D[r] = H(i0+r-1, j-1) + fsbt(q_{i0+r}, s_j)   (diagonal term, precomputed)
+//        F[r] = F(i0+r, j), e = E(i0, j), htop = H(i0-1, j)
+//        plo/phi -> profile rows of the NEXT column's residues (lo/hi subject)
+//   out: D[r] = H(i0+r-1, j) + fsbt(q_{i0+r}, s_{j+1}), F[r] = F(i0+r, j+1),
+//        e = E(i0+R, j); returns H(i0+R-1, j); hmax folds every H(i, j).
+// Per row (two cells): VIMNMX3 + 2 VIADDMNMX.RELU + 1/2 VIMNMX3 + PRMT on the
+// alu pipe, 2 VIADD.16x2 on the fma-side pipe (DESIGN.md §"Cell update").
+// The diagonal add is done one column ahead so ptxas cannot fuse it into an
+// alu-pipe VIADDMNMX, and D is updated in place (no register moves).  (Taking
+// E - alpha off the E chain costs a third VIADD.16x2 and measured 3% slower.)
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ uint32_t col16(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t& e, uint32_t htop,
+                                          const int8_t* __restrict__ plo, const int8_t* __restrict__ phi,
+                                          uint32_t na2, uint32_t nb2, uint32_t& hmax) {
+  uint32_t hprev = htop, hodd = 0u;
+  uint2 a = *reinterpret_cast<const uint2*>(plo);
+  uint2 b = *reinterpret_cast<const uint2*>(phi);
+#pragma unroll
+  for (int k = 0; k < R / 8; k++) {
+    uint2 an = a, bn = b;
+    if (k + 1 < R / 8) {
+      an = *reinterpret_cast<const uint2*>(plo + 8 * (k + 1));
+      bn = *reinterpret_cast<const uint2*>(phi + 8 * (k + 1));
+    }
+#pragma unroll
+    for (int rr = 0; rr < 8; rr++) {
+      const int r = 8 * k + rr;
+      const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);          // H(i,j) >= 0 since e, F >= 0
+      const uint32_t sn = prmt(rr < 4 ? a.x : a.y, rr < 4 ? b.x : b.y, sel_pair(rr & 3));
+      D[r] = __vadd2(hprev, sn);                                 // H(i-1,j) + fsbt(q_i, s_{j+1}); wraps only past LIMIT16
+      const uint32_t hb = __vadd2(h, nb2);                       // H(i,j) - beta
+      e = __viaddmax_s16x2_relu(e, na2, hb);                     // E(i+1,j) = max(E - alpha, H - beta, 0)
+      F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);               // F(i,j+1) = max(F - alpha, H - beta, 0)
+      if (rr & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
+      else hodd = h;
+      hprev = h;
+    }
+    a = an;
+    b = bn;
+  }
+  return hprev;
+}
+
+// Column of R <= 16 rows whose profile bytes for the lane (lo and hi subject)
+// are one 16-byte block each (the intra-task "blocked" profile: block b holds
+// query rows [b*R, b*R + R), zero-padded).  Same cell update as col16.
+template <int R>
+__device__ __forceinline__ uint32_t col16b(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t& e, uint32_t htop,
+                                           const uint4 a, const uint4 b, uint32_t na2, uint32_t nb2,
+                                           uint32_t& hmax) {
+  static_assert(R >= 2 && R <= 16, "blocked profile rows");
+  uint32_t hprev = htop, hodd = 0u;
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    const uint32_t wa = r < 4 ? a.x : r < 8 ? a.y : r < 12 ? a.z : a.w;
+    const uint32_t wb = r < 4 ? b.x : r < 8 ? b.y : r < 12 ? b.z : b.w;
+    const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);
+    const uint32_t sn = prmt(wa, wb, sel_pair(r & 3));
+    D[r] = __vadd2(hprev, sn);
+    const uint32_t hb = __vadd2(h, nb2);
+    e = __viaddmax_s16x2_relu(e, na2, hb);
+    F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+    if (r & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
+    else hodd = h;
+    hprev = h;
+  }
+  if (R & 1) hmax = __vmaxs2(hmax, hodd);
+  return hprev;
+}
+
+// Residue cursor over one lane's interleaved packed words (6 codes per word).
+
+// ---------------------------------------------------------------------------
+// Inter-task tile: rows [i0, i0+R) of the query against all columns of one
+// pair of subjects per lane (32 pairs = one 64-subject group per warp).
+// bnd[j] carries (E(i0,j), H(i0-1,j)) in and (E(i0+R,j), H(i0+R-1,j)) out
+// between tiles (the paper's "tiled SW computation").
+// ---------------------------------------------------------------------------
+// Two consecutive columns A = j and B = j+1 interleaved with a one-row skew:
+// step r does A(row r) and B(row r-1).  B(row r') only needs D[r'], F[r'] as
+// left by A(row r') and B's own E chain, so every step carries two independent
+// dependency chains (the fixed-latency "wait" stall of the single-column loop).
+template <int R>
+__device__ __forceinline__ void col16x2(uint32_t (&D)[R], uint32_t (&F)[R],
+                                        uint32_t& eA, uint32_t htopA, const int8_t* __restrict__ ploA,
+                                        const int8_t* __restrict__ phiA, uint32_t& eB, uint32_t htopB,
+                                        const int8_t* __restrict__ ploB, const int8_t* __restrict__ phiB,
+                                        uint32_t na2, uint32_t nb2, uint32_t& hmax, uint32_t& hlA,
+                                        uint32_t& hlB) {
+  uint32_t hpA = htopA, hpB = htopB, hoA = 0u, hoB = 0u;
+  uint2 aA = *reinterpret_cast<const uint2*>(ploA), bA = *reinterpret_cast<const uint2*>(phiA);
+  uint2 aB = *reinterpret_cast<const uint2*>(ploB), bB = *reinterpret_cast<const uint2*>(phiB);
+  uint2 aBn = aB, bBn = bB;
+#pragma unroll
+  for (int r = 0; r <= R; r++) {
+    if (r < R) {                                   // ---- column A, row r
+      const int rr = r & 7;
+      if (rr == 0 && r > 0) {
+        aA = *reinterpret_cast<const uint2*>(ploA + r);
+        bA = *reinterpret_cast<const uint2*>(phiA + r);
+      }
+      const uint32_t h = __vimax3_s16x2(D[r], eA, F[r]);
+      const uint32_t sn = prmt(rr < 4 ? aA.x : aA.y, rr < 4 ? bA.x : bA.y, sel_pair(rr & 3));
+      D[r] = __vadd2(hpA, sn);
+      const uint32_t hb = __vadd2(h, nb2);
+      eA = __viaddmax_s16x2_relu(eA, na2, hb);
+      F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+      if (rr & 1) hmax = __vimax3_s16x2(hmax, hoA, h);
+      else hoA = h;
+      hpA = h;
+    }
+    if (r >= 1) {                                  // ---- column B, row r-1
+      const int q = r - 1, rr = q & 7;
+      if (rr == 0 && q > 0) {
+        aB = aBn;
+        bB = bBn;
+      }
+      if (rr == 0 && q + 8 < R) {                  // B's next chunk, one chunk ahead
+        aBn = *reinterpret_cast<const uint2*>(ploB + q + 8);
+        bBn = *reinterpret_cast<const uint2*>(phiB + q + 8);
+      }
+      const uint32_t h = __vimax3_s16x2(D[q], eB, F[q]);
+      const uint32_t sn = prmt(rr < 4 ? aB.x : aB.y, rr < 4 ? bB.x : bB.y, sel_pair(rr & 3));
+      D[q] = __vadd2(hpB, sn);
+      const uint32_t hb = __vadd2(h, nb2);
+      eB = __viaddmax_s16x2_relu(eB, na2, hb);
+      F[q] = __viaddmax_s16x2_relu(F[q], na2, hb);
+      if (rr & 1) hmax = __vimax3_s16x2(hmax, hoB, h);
+      else hoB = h;
+      hpB = h;
+    }
+  }
+  hlA = hpA;
+  hlB = hpB;
+}
+
+// Packed residue pair (lo, hi codes) of column c of this lane: word c/6, field c%6.
+
+template <int R>
+__device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
+                                       const int8_t* __restrict__ prof, int stride, int i0,
+                                       uint2* __restrict__ bnd, bool first, bool last,
+                                       uint32_t na2, uint32_t nb2, uint32_t& hmax, int lane) {
+  if (ncols <= 0) return;
+  uint32_t D[R], F[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) { D[r] = 0u; F[r] = 0u; }
+  const uint2* lw = gw + lane;
+  const int nwords = (ncols + kResPerWord - 1) / kResPerWord;
+  const int8_t* pr = prof + i0;
+  {  // virtual column j = -1 (all-zero boundary): primes D[r] = fsbt(q_{i0+r}, s_0)
+    const uint2 w0 = lw[0];
+    uint32_t e0 = 0u;
+    col16<R>(D, F, e0, 0u, pr + (w0.x & 31u) * stride, pr + (w0.y & 31u) * stride, na2, nb2, hmax);
+  }
+  // Columns are taken two at a time (A = j, B = j+1).  The residue words of the
+  // next pair's "next columns" (j+3, j+4) and its boundary rows (j+2, j+3) are
+  // loaded one pair ahead into the registers they are consumed from.
+  const uint2 z = make_uint2(0u, 0u);
+  uint2 bE = first ? z : bnd[lane];
+  uint2 bO = (first || ncols < 2) ? z : bnd[32 + lane];
+  uint2 wA = res_word(lw, 1, nwords), wB = res_word(lw, 2, nwords);
+  int j = 0;
+  for (; j + 1 < ncols; j += 2) {
+    const int shA = res_shift(j + 1), shB = res_shift(j + 2);
+    uint32_t eA = bE.x, eB = bO.x, hlA, hlB;
+#ifdef SW_INTERLEAVE_COLUMNS
+    col16x2<R>(D, F, eA, bE.y, pr + ((wA.x >> shA) & 31u) * stride, pr + ((wA.y >> shA) & 31u) * stride,
+               eB, bO.y, pr + ((wB.x >> shB) & 31u) * stride, pr + ((wB.y >> shB) & 31u) * stride,
+               na2, nb2, hmax, hlA, hlB);
+#else
+    hlA = col16<R>(D, F, eA, bE.y, pr + ((wA.x >> shA) & 31u) * stride, pr + ((wA.y >> shA) & 31u) * stride,
+                   na2, nb2, hmax);
+    hlB = col16<R>(D, F, eB, bO.y, pr + ((wB.x >> shB) & 31u) * stride, pr + ((wB.y >> shB) & 31u) * stride,
+                   na2, nb2, hmax);
+#endif
+    wA = res_word(lw, j + 3, nwords);
+    wB = res_word(lw, j + 4, nwords);
+    if (!first && j + 2 < ncols) bE = bnd[(j + 2) * 32 + lane];
+    if (!first && j + 3 < ncols) bO = bnd[(j + 3) * 32 + lane];
+    if (!last) {
+      bnd[j * 32 + lane] = make_uint2(eA, hlA);
+      bnd[(j + 1) * 32 + lane] = make_uint2(eB, hlB);
+    }
+  }
+  if (j < ncols) {                                 // odd tail column
+    const int shA = res_shift(j + 1);
+    uint32_t e = bE.x;
+    const uint32_t hl = col16<R>(D, F, e, bE.y, pr + ((wA.x >> shA) & 31u) * stride,
+                                 pr + ((wA.y >> shA) & 31u) * stride, na2, nb2, hmax);
+    if (!last) bnd[j * 32 + lane] = make_uint2(e, hl);
+  }
+}
+
+template <int T, int R = T - 8>
+__device__ __forceinline__ void tile16_rem(int rem, const uint2* gw, int ncols, const int8_t* prof,
+                                           int stride, int i0, uint2* bnd, bool first,
+                                           uint32_t na2, uint32_t nb2, uint32_t& hmax, int lane) {
+  if constexpr (R >= 8) {
+    if (rem == R) tile16<R>(gw, ncols, prof, stride, i0, bnd, first, true, na2, nb2, hmax, lane);
+    else tile16_rem<T, R - 8>(rem, gw, ncols, prof, stride, i0, bnd, first, na2, nb2, hmax, lane);
+  }
+}
+
+// One 64-subject group, all query tiles (inter-task).  Not inlined, so the
+// register-hungry tile loop is allocated apart from the persistent queue logic.
+template <int T, bool SMEM>
+__device__ __forceinline__ uint32_t inter_group16(const uint2* __restrict__ gw, int ncols, const int8_t* __restrict__ gprof,
+                                               int stride, int m_pad, uint2* __restrict__ bnd, uint32_t na2,
+                                               uint32_t nb2, int lane) {
+  const int8_t* prof = prof_base<SMEM>(gprof);
+  const int nfull = m_pad / T, rem = m_pad - nfull * T;
+  uint32_t hmax = 0u;
+  for (int t = 0; t < nfull; t++)
+    tile16<T>(gw, ncols, prof, stride, t * T, bnd, t == 0, t == nfull - 1 && rem == 0, na2, nb2, hmax, lane);
+  if (rem) tile16_rem<T>(rem, gw, ncols, prof, stride, nfull * T, bnd, nfull == 0, na2, nb2, hmax, lane);
+  return hmax;
+}
+
+// ---------------------------------------------------------------------------
+// Intra-task wavefront for ONE pair of long subjects per warp (north star (c);
+// the role of the paper's intra-sequence model, with a
+// wavefront instead of Farrar striping).  Lane l owns query rows
+// [base + l*TR, base + (l+1)*TR) of a pass of 32*TR rows and processes column
+// j = s - l at step s; (E, H, next residue) flow to lane l+1 by SHFL.  The
+// last active lane's output row is kept in gbnd for the next pass.
+// Returns this lane's running max (to be reduced over the warp).
+// ---------------------------------------------------------------------------
+template <int TR, bool SMEM>
+__device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, int ncols,
+                                                 const int8_t* __restrict__ gprof, int stride, int m_pad,
+                                                 uint2* __restrict__ gbnd, long long gstride,
+                                                 uint32_t na2, uint32_t nb2, int lane) {
+  const int8_t* prof = prof_base<SMEM>(gprof);
+  uint32_t hmax = 0u;
+  const int nwords = (ncols + kResPerWord - 1) / kResPerWord;
+  int pass = 0;
+  for (int base = 0; base < m_pad; base += 32 * TR, pass++) {
+    const int nact = min(32, (m_pad - base + TR - 1) / TR);
+    const bool first = base == 0, last = base + 32 * TR >= m_pad;
+    const uint2* gin = gbnd + (long long)(pass & 1) * gstride;          // written by the previous pass
+    uint2* gout = gbnd + (long long)((pass + 1) & 1) * gstride;
+    const int8_t* pr = prof + (base / TR + lane) * 16;                 // this lane's 16-byte profile block
+    uint32_t D[TR], F[TR];
+#pragma unroll
+    for (int r = 0; r < TR; r++) { D[r] = 0u; F[r] = 0u; }
+    uint32_t e_out = 0u, h_out = 0u, r_out = 0u;
+    // Lane 0's per-step inputs (the residue pair of column s+1 and, after the
+    // first pass, the previous pass's boundary of column s) are fetched by all
+    // lanes for 32 steps at a time, one block ahead, and handed to lane 0 by
+    // SHFL -- no load latency on the wavefront's critical step.
+    auto fetch = [&](int sb, uint32_t& rp, uint2& gv) {
+      const int c = sb + 1 + lane;                                      // residue column for step sb + lane
+      const uint2 w = res_word(pw, c, nwords);
+      const int sh = res_shift(c);
+      rp = ((w.x >> sh) & 31u) | (((w.y >> sh) & 31u) << 5);
+      const int gc = sb + lane;                                         // boundary column for step sb + lane
+      gv = (!first && gc >= 0 && gc < ncols) ? gin[gc] : make_uint2(0u, 0u);
+    };
+    const int nsteps = ncols + nact;                                    // steps s = -1 .. ncols + nact - 2
+    uint32_t rp_cur, rp_nxt;
+    uint2 gv_cur, gv_nxt;
+    fetch(-1, rp_cur, gv_cur);
+    fetch(31, rp_nxt, gv_nxt);
+    __syncwarp();
+    for (int sb = -1; sb < nsteps - 1; sb += 32) {
+#pragma unroll 1
+      for (int t = 0; t < 32; t++) {
+        const int s = sb + t;
+        if (s >= nsteps - 1) break;
+        uint32_t e_in = __shfl_up_sync(0xffffffffu, e_out, 1);
+        uint32_t h_in = __shfl_up_sync(0xffffffffu, h_out, 1);
+        uint32_t r_in = __shfl_up_sync(0xffffffffu, r_out, 1);
+        const uint32_t r0 = __shfl_sync(0xffffffffu, rp_cur, t);
+        const uint32_t g0x = __shfl_sync(0xffffffffu, gv_cur.x, t);
+        const uint32_t g0y = __shfl_sync(0xffffffffu, gv_cur.y, t);
+        const int j = s - lane;
+        if (lane == 0) {
+          r_in = r0;                                                    // residues of column j+1
+          e_in = g0x;                                                   // E(base, j), H(base-1, j) (0 on pass 0 / j < 0)
+          h_in = g0y;
+        }
+        if (lane < nact && j >= -1 && j < ncols) {
+          uint32_t e = e_in;
+          const uint4 pa = *reinterpret_cast<const uint4*>(pr + (r_in & 31u) * stride);
+          const uint4 pb = *reinterpret_cast<const uint4*>(pr + (r_in >> 5) * stride);
+          const uint32_t hl = col16b<TR>(D, F, e, h_in, pa, pb, na2, nb2, hmax);
+          e_out = e;
+          h_out = hl;
+          r_out = r_in;
+          if (!last && lane == nact - 1 && j >= 0) gout[j] = make_uint2(e, hl);
+        }
+      }
+      rp_cur = rp_nxt;
+      gv_cur = gv_nxt;
+      fetch(sb + 64, rp_nxt, gv_nxt);
+    }
+    __syncwarp();
+  }
+  return hmax;
+}
+
+
+template <int T, bool SMEM, int NT, bool BIG = false, bool STATIC = false>
+__global__ void __launch_bounds__(NT, 1)
+k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
+          const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
+          const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
+          uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
+          int* __restrict__ score_sorted, uint8_t* __restrict__ flag, long long big_off,
+          long long big_cols, int n_big) {
+  extern __shared__ __align__(16) int8_t sprof[];
+  __shared__ int s_split;
+  if (n_groups_dev) n_groups = *n_groups_dev;   // mini-group layout of a rerun: size known on device only
+  if (threadIdx.x == 0) s_split = split_groups(groups, n_groups, cut);
+  __syncthreads();
+  const int n_items = s_split;
+  if (n_items <= 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
+  if (SMEM) load_profile_smem(sprof, gprof, stride);
+  const int lane = threadIdx.x & 31;
+  const long long own = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
+  uint2* const own_bnd = scratch + own;
+  const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
+  int it_static = 0;
+  for (;;) {
+    int item = 0;
+    if constexpr (STATIC) {
+      // f4 ablation of the paper's OpenMP "static" schedule: item w + t*W
+      item = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) + it_static++ * gridDim.x * (blockDim.x >> 5);
+    } else {
+      if (lane == 0) item = atomicAdd(counter, 1);
+      item = __shfl_sync(0xffffffffu, item, 0);
+    }
+    if (item >= n_items) break;
+    const int g = n_items - 1 - item;
+    const GroupDesc gd = groups[g];
+    // the n_big longest groups (the first items) are wider than a warp's slab:
+    // each has a boundary slab of its own, big_off words from `scratch` (one
+    // base pointer keeps the slab accesses of the hot loop __restrict__)
+    uint2* bnd = own_bnd;
+    if constexpr (BIG) bnd = scratch + (item < n_big ? big_off + (long long)item * big_cols * 32 : own);
+    const uint32_t hmax = inter_group16<T, SMEM>(words + gd.base, gd.ncols, gprof, stride, m_pad, bnd, na2, nb2, lane);
+    emit_pair(hmax, g, 2 * lane, gd.count, limit, pos_map, score_sorted, flag);
+  }
+  // Launched as the programmatic dependent of k_intra16 (same stream): do not
+  // retire before that grid has completed, so the stream's later work sees its
+  // scores.  A no-op when there is no primary grid.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Intra-task pass over groups [split, n_groups): one subject PAIR per work item,
+// longest first, aligned by the lane wavefront.  A kernel of its own (own
+// register allocation), launched on a second stream beside k_inter16.
+template <int TR, bool SMEM>
+__global__ void __launch_bounds__(kInterThreads, 1)
+k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
+          const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
+          const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
+          uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
+          int* __restrict__ score_sorted, uint8_t* __restrict__ flag) {
+  // The inter-task kernel may start beside this one (programmatic dependent
+  // launch): it only reads what was complete before this grid started.
+  asm volatile("griddepcontrol.launch_dependents;");
+  extern __shared__ __align__(16) int8_t sprof[];
+  __shared__ int s_split;
+  if (n_groups_dev) n_groups = *n_groups_dev;
+  if (threadIdx.x == 0) s_split = split_groups(groups, n_groups, cut);
+  __syncthreads();
+  const int split = s_split;
+  const int n_items = (n_groups - split) * 32;
+  if (n_items <= 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
+  if (SMEM) load_profile_smem(sprof, gprof, stride);
+  const int lane = threadIdx.x & 31;
+  uint2* bnd = scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
+  const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(counter, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    const int g = n_groups - 1 - item / 32;
+    const int p = 31 - item % 32;
+    const GroupDesc gd = groups[g];
+    if (2 * p >= gd.count) continue;
+    uint32_t hm = intra_pair16<TR, SMEM>(words + gd.base + p, gd.ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
+                                         na2, nb2, lane);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hm = __vmaxs2(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+    if (lane == 0) emit_pair(hm, g, 2 * p, gd.count, limit, pos_map, score_sorted, flag);
+  }
+  // When launched as a programmatic dependent (a chain of intra-task passes in
+  // sw_search_batch), retire only after the primary grid: a no-op otherwise.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+
+}  // namespace swk

@@ -1,0 +1,217 @@
+// sw_rank.cuh -- a6: scatter to input order and exact top-k
+// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+#pragma once
+#include "sw_common.cuh"
+
+namespace swk {
+
+// ---------------------------------------------------------------------------
+// (iv) finalize: scatter to input order and build unique 64-bit ranking keys
+// (score << 32 | ~gid): "sort all alignment scores in descending order"
+// (PAPER.md:55), ties by ascending global id (reading R7).
+// ---------------------------------------------------------------------------
+__global__ void k_finalize(const int* __restrict__ score_sorted, const int* __restrict__ perm, int n,
+                           const long long* __restrict__ gid, int* __restrict__ scores_out,
+                           unsigned long long* __restrict__ keys) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const int idx = perm[p];
+    const int s = score_sorted[p];
+    if (scores_out) scores_out[idx] = s;
+    const unsigned long long id = gid ? (unsigned long long)gid[idx] : (unsigned long long)idx;
+    keys[p] = ((unsigned long long)(unsigned)s << 32) | (0xffffffffull - id);
+  }
+}
+
+struct SelState {
+  unsigned long long prefix, mask;
+  long long kk;     // rank (1-based) still to find inside the current prefix
+};
+
+__global__ void k_sel_init(SelState* st, long long k) {
+  if (threadIdx.x == 0) {
+    st->prefix = 0ull;
+    st->mask = 0ull;
+    st->kk = k;
+  }
+}
+
+// Radix select of the k-th largest key, 8 bits per pass (most significant first).
+__global__ void k_sel_hist(const unsigned long long* __restrict__ keys, int n,
+                           const SelState* __restrict__ st, int shift, unsigned* __restrict__ hist) {
+  __shared__ unsigned sh[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
+  __syncthreads();
+  const unsigned long long prefix = st->prefix, mask = st->mask;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const unsigned long long key = keys[p];
+    if ((key & mask) == prefix) atomicAdd(&sh[(key >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x)
+    if (sh[t]) atomicAdd(&hist[t], sh[t]);
+}
+
+__global__ void __launch_bounds__(256) k_sel_pick(SelState* st, int shift, unsigned* hist) {
+  // digit d is chosen so that (# keys with digit > d) < kk <= (# keys with digit >= d);
+  // suffix sums over the 256 bins by a block-wide scan (descending digit order)
+  __shared__ long long suf[256];
+  const int t = threadIdx.x;
+  const int d = 255 - t;                       // thread t holds digit 255 - t
+  long long v = hist[d];
+  suf[t] = v;
+  __syncthreads();
+  for (int off = 1; off < 256; off <<= 1) {
+    const long long add = t >= off ? suf[t - off] : 0;
+    __syncthreads();
+    suf[t] += add;
+    __syncthreads();
+  }
+  const long long kk = st->kk;
+  const long long incl = suf[t], excl = incl - v;   // keys with digit >= d, > d
+  __syncthreads();
+  if (excl < kk && kk <= incl) {
+    st->kk = kk - excl;
+    st->prefix |= (unsigned long long)d << shift;
+    st->mask |= 255ull << shift;
+  }
+  hist[d] = 0;
+}
+
+__global__ void k_sel_compact(const unsigned long long* __restrict__ keys, int n,
+                              const SelState* __restrict__ st, int take_all,
+                              unsigned long long* __restrict__ out, int* __restrict__ count) {
+  const unsigned long long thr = take_all ? 0ull : st->prefix;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const unsigned long long key = keys[p];
+    if (key >= thr) out[atomicAdd(count, 1)] = key;
+  }
+}
+
+// Single-CTA bitonic sort (descending) of cnt <= 4096 keys, then decode.
+__global__ void __launch_bounds__(1024) k_topk_small(const unsigned long long* __restrict__ cand,
+                                                     int cnt, int k, long long* __restrict__ out_ids,
+                                                     int* __restrict__ out_scores) {
+  __shared__ unsigned long long s[4096];
+  int n2 = 1;
+  while (n2 < cnt) n2 <<= 1;
+  for (int t = threadIdx.x; t < n2; t += blockDim.x) s[t] = t < cnt ? cand[t] : 0ull;
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+        const int u = t ^ stride;
+        if (u > t) {
+          const bool desc = (t & size) == 0;
+          const unsigned long long a = s[t], b = s[u];
+          if (desc ? (a < b) : (a > b)) { s[t] = b; s[u] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    if (t < cnt) {
+      const unsigned long long key = s[t];
+      if (out_ids) out_ids[t] = (long long)(0xffffffffull - (key & 0xffffffffull));
+      if (out_scores) out_scores[t] = (int)(key >> 32);
+    } else {
+      if (out_ids) out_ids[t] = -1;
+      if (out_scores) out_scores[t] = -1;
+    }
+  }
+}
+
+// Small databases (n <= 65,536, min(k, n) <= 4,096): the whole ranking in ONE
+// CTA -- radix select of the k-th largest unique key (8 bits per pass, smem
+// histogram), compaction of the k keys above it, bitonic sort, decode --
+// instead of the 19-launch multi-CTA path.
+__global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* __restrict__ keys, int n, int k,
+                                                     long long* __restrict__ out_ids, int* __restrict__ out_scores) {
+  __shared__ unsigned long long s[4096];
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long sh_prefix, sh_mask;
+  __shared__ long long sh_kk;
+  __shared__ int sh_cnt;
+  const int cnt = min(k, n);
+  unsigned long long thr = 0ull;
+  if (k < n) {
+    if (threadIdx.x == 0) { sh_prefix = 0ull; sh_mask = 0ull; sh_kk = k; }
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0u;
+      __syncthreads();
+      const unsigned long long prefix = sh_prefix, mask = sh_mask;
+      for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        const unsigned long long key = keys[p];
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {                                  // digit with (# > d) < kk <= (# >= d)
+        long long above = 0;
+        const long long kk = sh_kk;
+        for (int d = 255; d >= 0; d--) {
+          const long long c = hist[d];
+          if (above < kk && kk <= above + c) {
+            sh_kk = kk - above;
+            sh_prefix = prefix | ((unsigned long long)d << shift);
+            sh_mask = mask | (255ull << shift);
+            break;
+          }
+          above += c;
+        }
+      }
+      __syncthreads();
+    }
+    thr = sh_prefix;                                           // the k-th largest key (keys are unique)
+  }
+  if (threadIdx.x == 0) sh_cnt = 0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    const unsigned long long key = keys[p];
+    if (key >= thr) s[atomicAdd(&sh_cnt, 1)] = key;
+  }
+  __syncthreads();
+  int n2 = 1;
+  while (n2 < cnt) n2 <<= 1;
+  for (int t = cnt + threadIdx.x; t < n2; t += blockDim.x) s[t] = 0ull;
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+        const int u = t ^ stride;
+        if (u > t) {
+          const bool desc = (t & size) == 0;
+          const unsigned long long a = s[t], b = s[u];
+          if (desc ? (a < b) : (a > b)) { s[t] = b; s[u] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    if (t < cnt) {
+      const unsigned long long key = s[t];
+      if (out_ids) out_ids[t] = (long long)(0xffffffffull - (key & 0xffffffffull));
+      if (out_scores) out_scores[t] = (int)(key >> 32);
+    } else {
+      if (out_ids) out_ids[t] = -1;
+      if (out_scores) out_scores[t] = -1;
+    }
+  }
+}
+
+__global__ void k_topk_decode(const unsigned long long* __restrict__ sorted, int cnt, int k,
+                              long long* __restrict__ out_ids, int* __restrict__ out_scores) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < k; t += gridDim.x * blockDim.x) {
+    if (t < cnt) {
+      const unsigned long long key = sorted[t];
+      if (out_ids) out_ids[t] = (long long)(0xffffffffull - (key & 0xffffffffull));
+      if (out_scores) out_scores[t] = (int)(key >> 32);
+    } else {
+      if (out_ids) out_ids[t] = -1;
+      if (out_scores) out_scores[t] = -1;
+    }
+  }
+}
+
+
+}  // namespace swk
