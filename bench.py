@@ -193,7 +193,7 @@ def traffic_model(lengths, m: int, n_warps: int = SMS * 12, tile_rows: int = 48)
     ncols = ls[np.minimum(np.arange(0, ls.size, 64) + 63, ls.size - 1)]
     m_pad = (m + 7) // 8 * 8
     db_bytes = int(((ncols + 5) // 6 * 32 * 8).sum())
-    cut = max(128, int(ls.sum()) // (64 * n_warps))
+    cut = max(64, int(ls.sum()) // (64 * n_warps))
     inter, intra = ncols[ncols <= cut], ncols[ncols > cut]
     tiles = -(-m_pad // tile_rows)
     tr = 8 if m_pad <= 256 else 16

@@ -231,11 +231,51 @@ __device__ __forceinline__ uint32_t inter_group16(const uint2* __restrict__ gw, 
 // Intra-task wavefront for ONE pair of long subjects per warp (north star (c);
 // the role of the paper's intra-sequence model, with a
 // wavefront instead of Farrar striping).  Lane l owns query rows
-// [base + l*TR, base + (l+1)*TR) of a pass of 32*TR rows and processes column
-// j = s - l at step s; (E, H, next residue) flow to lane l+1 by SHFL.  The
-// last active lane's output row is kept in gbnd for the next pass.
-// Returns this lane's running max (to be reduced over the warp).
+// [base + l*TR, base + (l+1)*TR) of a pass of 32*TR rows.  Columns are taken
+// two at a time: at step s lane l aligns the column pair k = s - l, i.e.
+// columns A = 2k-1 and B = 2k (column -1 is the all-zero boundary that primes
+// the diagonal terms), interleaved with a one-row skew so every step carries
+// two independent dependency chains; (E, H) of both columns and the next
+// residues flow to lane l+1 by SHFL.  The last active lane's output rows are
+// kept in gbnd for the next pass.  Returns this lane's running max.
 // ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ void col16b_x2(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t& eA, uint32_t htopA,
+                                          const uint4 a1, const uint4 b1, uint32_t& eB, uint32_t htopB,
+                                          const uint4 a2, const uint4 b2, uint32_t na2, uint32_t nb2,
+                                          uint32_t& hmax, uint32_t& hlA, uint32_t& hlB) {
+  uint32_t hpA = htopA, hpB = htopB, hA = 0u;
+#pragma unroll
+  for (int r = 0; r <= R; r++) {
+    if (r < R) {                                                  // column A, row r
+      const uint32_t wa = r < 4 ? a1.x : r < 8 ? a1.y : r < 12 ? a1.z : a1.w;
+      const uint32_t wb = r < 4 ? b1.x : r < 8 ? b1.y : r < 12 ? b1.z : b1.w;
+      hA = __vimax3_s16x2(D[r], eA, F[r]);
+      D[r] = __vadd2(hpA, prmt(wa, wb, sel_pair(r & 3)));         // H(i-1,A) + fsbt(q_i, s_B)
+      const uint32_t hb = __vadd2(hA, nb2);
+      eA = __viaddmax_s16x2_relu(eA, na2, hb);
+      F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+      hpA = hA;
+      if (r == 0) hmax = __vmaxs2(hmax, hA);                     // rows 1.. are folded with column B
+    }
+    if (r >= 1) {                                                 // column B, row r-1
+      const int q = r - 1;
+      const uint32_t wa = q < 4 ? a2.x : q < 8 ? a2.y : q < 12 ? a2.z : a2.w;
+      const uint32_t wb = q < 4 ? b2.x : q < 8 ? b2.y : q < 12 ? b2.z : b2.w;
+      const uint32_t h = __vimax3_s16x2(D[q], eB, F[q]);
+      D[q] = __vadd2(hpB, prmt(wa, wb, sel_pair(q & 3)));         // H(i-1,B) + fsbt(q_i, s_{B+1})
+      const uint32_t hb = __vadd2(h, nb2);
+      eB = __viaddmax_s16x2_relu(eB, na2, hb);
+      F[q] = __viaddmax_s16x2_relu(F[q], na2, hb);
+      if (r < R) hmax = __vimax3_s16x2(hmax, h, hA);             // H(q, B) and H(r, A)
+      else hmax = __vmaxs2(hmax, h);
+      hpB = h;
+    }
+  }
+  hlA = hpA;
+  hlB = hpB;
+}
+
 template <int TR, bool SMEM>
 __device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, int ncols,
                                                  const int8_t* __restrict__ gprof, int stride, int m_pad,
@@ -244,6 +284,7 @@ __device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, i
   const int8_t* prof = prof_base<SMEM>(gprof);
   uint32_t hmax = 0u;
   const int nwords = (ncols + kResPerWord - 1) / kResPerWord;
+  const int K = (ncols + 2) / 2;                                        // column pairs (-1,0), (1,2), ...
   int pass = 0;
   for (int base = 0; base < m_pad; base += 32 * TR, pass++) {
     const int nact = min(32, (m_pad - base + TR - 1) / TR);
@@ -254,56 +295,71 @@ __device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, i
     uint32_t D[TR], F[TR];
 #pragma unroll
     for (int r = 0; r < TR; r++) { D[r] = 0u; F[r] = 0u; }
-    uint32_t e_out = 0u, h_out = 0u, r_out = 0u;
-    // Lane 0's per-step inputs (the residue pair of column s+1 and, after the
-    // first pass, the previous pass's boundary of column s) are fetched by all
-    // lanes for 32 steps at a time, one block ahead, and handed to lane 0 by
-    // SHFL -- no load latency on the wavefront's critical step.
-    auto fetch = [&](int sb, uint32_t& rp, uint2& gv) {
-      const int c = sb + 1 + lane;                                      // residue column for step sb + lane
-      const uint2 w = res_word(pw, c, nwords);
-      const int sh = res_shift(c);
-      rp = ((w.x >> sh) & 31u) | (((w.y >> sh) & 31u) << 5);
-      const int gc = sb + lane;                                         // boundary column for step sb + lane
-      gv = (!first && gc >= 0 && gc < ncols) ? gin[gc] : make_uint2(0u, 0u);
+    uint32_t eA_out = 0u, hA_out = 0u, eB_out = 0u, hB_out = 0u, r_out = 0u;
+    // Lane 0's per-step inputs for pair k (residues of columns 2k and 2k+1, and
+    // after the first pass the previous pass's boundary of columns 2k-1, 2k) are
+    // fetched by all lanes 32 pairs at a time, one block ahead, and handed over by SHFL.
+    auto fetch = [&](int kb, uint32_t& rp, uint2& ga, uint2& gb) {
+      const int k = kb + lane;
+      const int c0 = 2 * k, c1 = 2 * k + 1;
+      const uint2 w0 = res_word(pw, c0, nwords), w1 = res_word(pw, c1, nwords);
+      const int s0 = res_shift(c0), s1 = res_shift(c1);
+      rp = ((w0.x >> s0) & 31u) | (((w0.y >> s0) & 31u) << 5) | (((w1.x >> s1) & 31u) << 10) |
+           (((w1.y >> s1) & 31u) << 15);
+      const int ca = 2 * k - 1, cb = 2 * k;
+      ga = (!first && ca >= 0 && ca < ncols) ? gin[ca] : make_uint2(0u, 0u);
+      gb = (!first && cb < ncols) ? gin[cb] : make_uint2(0u, 0u);
     };
-    const int nsteps = ncols + nact;                                    // steps s = -1 .. ncols + nact - 2
+    const int nsteps = K + nact - 1;
     uint32_t rp_cur, rp_nxt;
-    uint2 gv_cur, gv_nxt;
-    fetch(-1, rp_cur, gv_cur);
-    fetch(31, rp_nxt, gv_nxt);
+    uint2 ga_cur, gb_cur, ga_nxt, gb_nxt;
+    fetch(0, rp_cur, ga_cur, gb_cur);
+    fetch(32, rp_nxt, ga_nxt, gb_nxt);
     __syncwarp();
-    for (int sb = -1; sb < nsteps - 1; sb += 32) {
+    for (int sb = 0; sb < nsteps; sb += 32) {
 #pragma unroll 1
       for (int t = 0; t < 32; t++) {
         const int s = sb + t;
-        if (s >= nsteps - 1) break;
-        uint32_t e_in = __shfl_up_sync(0xffffffffu, e_out, 1);
-        uint32_t h_in = __shfl_up_sync(0xffffffffu, h_out, 1);
+        if (s >= nsteps) break;
+        uint32_t eA = __shfl_up_sync(0xffffffffu, eA_out, 1);
+        uint32_t hA = __shfl_up_sync(0xffffffffu, hA_out, 1);
+        uint32_t eB = __shfl_up_sync(0xffffffffu, eB_out, 1);
+        uint32_t hB = __shfl_up_sync(0xffffffffu, hB_out, 1);
         uint32_t r_in = __shfl_up_sync(0xffffffffu, r_out, 1);
         const uint32_t r0 = __shfl_sync(0xffffffffu, rp_cur, t);
-        const uint32_t g0x = __shfl_sync(0xffffffffu, gv_cur.x, t);
-        const uint32_t g0y = __shfl_sync(0xffffffffu, gv_cur.y, t);
-        const int j = s - lane;
+        const uint32_t gax = __shfl_sync(0xffffffffu, ga_cur.x, t), gay = __shfl_sync(0xffffffffu, ga_cur.y, t);
+        const uint32_t gbx = __shfl_sync(0xffffffffu, gb_cur.x, t), gby = __shfl_sync(0xffffffffu, gb_cur.y, t);
+        const int k = s - lane;
         if (lane == 0) {
-          r_in = r0;                                                    // residues of column j+1
-          e_in = g0x;                                                   // E(base, j), H(base-1, j) (0 on pass 0 / j < 0)
-          h_in = g0y;
+          r_in = r0;                                                    // residues of columns 2k, 2k+1
+          eA = gax;                                                     // E(base, A), H(base-1, A)
+          hA = gay;
+          eB = gbx;                                                     // E(base, B), H(base-1, B)
+          hB = gby;
         }
-        if (lane < nact && j >= -1 && j < ncols) {
-          uint32_t e = e_in;
-          const uint4 pa = *reinterpret_cast<const uint4*>(pr + (r_in & 31u) * stride);
-          const uint4 pb = *reinterpret_cast<const uint4*>(pr + (r_in >> 5) * stride);
-          const uint32_t hl = col16b<TR>(D, F, e, h_in, pa, pb, na2, nb2, hmax);
-          e_out = e;
-          h_out = hl;
+        if (lane < nact && k >= 0 && k < K) {
+          const uint4 a1 = *reinterpret_cast<const uint4*>(pr + (r_in & 31u) * stride);
+          const uint4 b1 = *reinterpret_cast<const uint4*>(pr + ((r_in >> 5) & 31u) * stride);
+          const uint4 a2 = *reinterpret_cast<const uint4*>(pr + ((r_in >> 10) & 31u) * stride);
+          const uint4 b2 = *reinterpret_cast<const uint4*>(pr + ((r_in >> 15) & 31u) * stride);
+          uint32_t hlA, hlB;
+          col16b_x2<TR>(D, F, eA, hA, a1, b1, eB, hB, a2, b2, na2, nb2, hmax, hlA, hlB);
+          eA_out = eA;
+          hA_out = hlA;
+          eB_out = eB;
+          hB_out = hlB;
           r_out = r_in;
-          if (!last && lane == nact - 1 && j >= 0) gout[j] = make_uint2(e, hl);
+          if (!last && lane == nact - 1) {
+            const int ca = 2 * k - 1, cb = 2 * k;
+            if (ca >= 0) gout[ca] = make_uint2(eA, hlA);
+            if (cb < ncols) gout[cb] = make_uint2(eB, hlB);
+          }
         }
       }
       rp_cur = rp_nxt;
-      gv_cur = gv_nxt;
-      fetch(sb + 64, rp_nxt, gv_nxt);
+      ga_cur = ga_nxt;
+      gb_cur = gb_nxt;
+      fetch(sb + 64, rp_nxt, ga_nxt, gb_nxt);
     }
     __syncwarp();
   }
@@ -389,10 +445,16 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   const int lane = threadIdx.x & 31;
   uint2* bnd = scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
   const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
-  for (;;) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(counter, 1);
-    item = __shfl_sync(0xffffffffu, item, 0);
+  // First items are dealt across the SMs (warp k of CTA b takes item k*gridDim.x + b),
+  // so the longest pairs -- the wavefront's critical paths -- do not share an SM;
+  // the rest come longest-first from the counter.
+  const int n_warps = gridDim.x * (blockDim.x >> 5);
+  int item = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  for (;; item = -1) {
+    if (item < 0) {
+      if (lane == 0) item = n_warps + atomicAdd(counter, 1);
+      item = __shfl_sync(0xffffffffu, item, 0);
+    }
     if (item >= n_items) break;
     const int g = n_groups - 1 - item / 32;
     const int p = 31 - item % 32;
