@@ -353,3 +353,30 @@ def test_empty_database():
         assert r.scores.size == 0
         assert r.topk_ids.tolist() == [-1] * 4 and r.topk_scores.tolist() == [-1] * 4
         assert g.align(_query(50, 3), B62, 2, 12, []) == []
+
+
+def test_destroy_releases_device_memory():
+    """Every buffer a handle allocates (search, batch, traceback, streaming,
+    wide-group slabs) is released by sw_db_destroy: free device memory comes back."""
+    import torch
+    rng = np.random.default_rng(99)
+    db = random_db(99, np.concatenate([rng.integers(1, 900, 3000), [7000, 9000]]))
+    qs = [_query(m, 99) for m in (300, 290, 120)]
+
+    def cycle(residency):
+        with sw.Database.from_synth(db, device=0, residency=residency, chunk_mb=1, long_threshold=64) as g:
+            g.search(qs[0], B62, 2, 12, k=5)
+            if residency == 0:
+                g.search_batch(qs, B62, 2, 12, k=5)
+            r = g.search(qs[2], B62, 2, 12, k=3)
+            g.align(qs[2], B62, 2, 12, r.topk_ids)
+        torch.cuda.synchronize()
+
+    cycle(0)
+    cycle(1)                                           # warm up the CUDA context and allocator
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(4):
+        cycle(0)
+        cycle(1)
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 64 << 20, f"{(free0 - free1) >> 20} MiB not released"
