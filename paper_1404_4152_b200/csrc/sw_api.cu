@@ -99,6 +99,7 @@ constexpr int kMaxSmemProfile = 200 * 1024;
 // Shape of the intra-task wavefront's blocked profile: TR rows per lane, the
 // fewest that put the query in one 32-lane pass (TR in {4, 6, 8, 12, 16}; longer
 // queries take several passes of 16 rows per lane), so few lanes idle.
+// (TR in {4, 5, 6, 7, 8, 10, 12, 14, 16}.)
 struct IntraShape {
   int tr, nblk, rowstride;
   size_t bytes;
@@ -107,7 +108,7 @@ struct IntraShape {
 IntraShape intra_shape(int m_pad) {
   const int need = (m_pad + 31) / 32;
   IntraShape sh;
-  sh.tr = need <= 4 ? 4 : need <= 6 ? 6 : need <= 8 ? 8 : need <= 12 ? 12 : 16;
+  sh.tr = need <= 4 ? 4 : need <= 8 ? need : need <= 10 ? 10 : need <= 12 ? 12 : need <= 14 ? 14 : 16;
   sh.nblk = (m_pad + sh.tr - 1) / sh.tr;
   sh.rowstride = sh.nblk * 16;
   sh.bytes = (size_t)swk::kProfRows * sh.rowstride;
@@ -117,9 +118,13 @@ IntraShape intra_shape(int m_pad) {
 void* intra_kernel(const IntraShape& sh) {
   switch (sh.tr) {
     case 4: return sh.smem ? (void*)swk::k_intra16<4, true> : (void*)swk::k_intra16<4, false>;
+    case 5: return sh.smem ? (void*)swk::k_intra16<5, true> : (void*)swk::k_intra16<5, false>;
     case 6: return sh.smem ? (void*)swk::k_intra16<6, true> : (void*)swk::k_intra16<6, false>;
+    case 7: return sh.smem ? (void*)swk::k_intra16<7, true> : (void*)swk::k_intra16<7, false>;
     case 8: return sh.smem ? (void*)swk::k_intra16<8, true> : (void*)swk::k_intra16<8, false>;
+    case 10: return sh.smem ? (void*)swk::k_intra16<10, true> : (void*)swk::k_intra16<10, false>;
     case 12: return sh.smem ? (void*)swk::k_intra16<12, true> : (void*)swk::k_intra16<12, false>;
+    case 14: return sh.smem ? (void*)swk::k_intra16<14, true> : (void*)swk::k_intra16<14, false>;
     default: return sh.smem ? (void*)swk::k_intra16<16, true> : (void*)swk::k_intra16<16, false>;
   }
 }
