@@ -380,3 +380,33 @@ def test_destroy_releases_device_memory():
         cycle(1)
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 < 64 << 20, f"{(free0 - free1) >> 20} MiB not released"
+
+
+def test_concurrent_handles_and_threads():
+    """Two handles searched from four host threads at once (the C ABI serialises
+    each handle, distinct handles run independently): every result exact."""
+    import threading
+    rng = np.random.default_rng(123)
+    dbs = [random_db(123 + t, rng.integers(1, 800, 1500)) for t in range(2)]
+    qs = [_query(m, 123) for m in (150, 400)]
+    refs = {(d, i): oracle.db_scores(q, dbs[d], B62, 2, 12) for d in range(2) for i, q in enumerate(qs)}
+    handles = [sw.Database.from_synth(d, device=0) for d in dbs]
+    errors = []
+
+    def worker(d, i):
+        try:
+            for _ in range(5):
+                r = handles[d].search(qs[i], B62, 2, 12, k=5)
+                if not np.array_equal(r.scores, refs[(d, i)]):
+                    errors.append((d, i))
+        except Exception as e:                          # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(d, i)) for d in range(2) for i in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for h in handles:
+        h.close()
+    assert not errors, errors
