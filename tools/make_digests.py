@@ -26,6 +26,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("config")
 ap.add_argument("--m", type=int, default=None)
 ap.add_argument("--threads", type=int, default=None)
+ap.add_argument("--out", default=None, help="output directory (default tests/golden/digests)")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 m = a.m or cfg.qlens[0]
@@ -33,7 +34,7 @@ q = make_query(cfg, m)
 M = cfg.matrix32()
 lk = db_lengths(cfg)
 n = cfg.n_seqs
-out = os.path.join(ROOT, "tests", "golden", "digests", f"{cfg.name}_m{m}.json")
+out = os.path.join(a.out or os.path.join(ROOT, "tests", "golden", "digests"), f"{cfg.name}_m{m}.json")
 os.makedirs(os.path.dirname(out), exist_ok=True)
 t0 = time.time()
 digests, top_ids, top_scores, manifests = [], np.zeros(0, np.int64), np.zeros(0, np.int32), []
