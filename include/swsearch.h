@@ -66,8 +66,12 @@ typedef struct sw_db sw_db; /* opaque; owns its device memory */
 typedef struct sw_opts {
   int32_t device;         /* CUDA device ordinal; -1 = the caller's current device */
   int32_t first_stage;    /* lane width of the first pass: 8, 16 (default) or 32 */
-  int32_t long_threshold; /* subjects longer than this use the intra-task wavefront kernel;
-                             0 = library default, -1 = never (all inter-task) */
+  int32_t long_threshold; /* 64-subject groups wider than this many columns are aligned pair
+                             by pair by the intra-task wavefront kernel; 0 = library default
+                             (max(64, ~one warp's share of the residues)), -1 = none (all
+                             inter-task; groups wider than a warp's boundary slab then get
+                             slabs of their own, up to 2,048 groups / 8 GiB, the rest stay
+                             intra-task).  Results never depend on it. */
   int32_t verbose;        /* 0 = silent */
   int32_t residency;      /* 0 = packed database resident in device memory (default);
                              1 = kept in pinned host memory and streamed to the device
