@@ -112,3 +112,51 @@ def test_encode_matches_alphabet_table():
     with pytest.raises(sw.SwError) as e:
         sw.encode("AR1N")
     assert e.value.code == sw.SW_EINVAL and b"position 2" in sw.lib().sw_last_error()
+
+
+def _crafted_index(seed=11, n=150):
+    import index_file
+    rng = np.random.default_rng(seed)
+    lengths = rng.integers(0, 90, size=n).astype(np.int32)
+    offsets = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.int64)
+    residues = rng.integers(0, 24, size=int(lengths.sum())).astype(np.uint8)
+    gids = rng.permutation(10 * n)[:n].astype(np.int64)
+    return index_file, index_file.build(residues, offsets, lengths, gids)
+
+
+@pytest.mark.parametrize("corrupt", ["none", "perm_dup", "perm_range", "len_order", "group_count", "group_ncols",
+                                     "code_25", "top_bits", "gid_range", "sum_len", "max_len"])
+def test_db_load_validates_index_contents(tmp_path, corrupt):
+    """A file written from the layout's definition passes the loader's host-side checks (on CPU the load then
+    stops at the device: SW_ECUDA); each corruption of its contents is SW_EINVAL before any device work."""
+    index_file, sec = _crafted_index()
+    hdr = {}
+    if corrupt == "perm_dup":
+        sec["perm"][5] = sec["perm"][6]
+    elif corrupt == "perm_range":
+        sec["perm"][0] = sec["len_sorted"].size
+    elif corrupt == "len_order":
+        sec["len_sorted"][[3, 140]] = sec["len_sorted"][[140, 3]]
+    elif corrupt == "group_count":
+        b, c, k = sec["groups"][0]
+        sec["groups"][0] = (b, c, k - 1)
+    elif corrupt == "group_ncols":
+        b, c, k = sec["groups"][1]
+        sec["groups"][1] = (b, c - 1, k)
+    elif corrupt == "code_25":
+        sec["words"][7] = (sec["words"][7] & ~np.uint32(31 << 10)) | np.uint32(25 << 10)
+    elif corrupt == "top_bits":
+        sec["words"][9] |= np.uint32(1 << 31)
+    elif corrupt == "gid_range":
+        sec["gids"][4] = -3
+    elif corrupt == "sum_len":
+        hdr["sum_len"] = int(sec["len_sorted"].sum()) + 1
+    elif corrupt == "max_len":
+        hdr["max_len"] = int(sec["len_sorted"][-1]) + 1
+    path = str(tmp_path / "crafted.swb")
+    index_file.write(path, sec, hdr)
+    if corrupt == "none" and __import__("torch").cuda.is_available():
+        pytest.skip("loads for real on a GPU box (tests/test_gpu_parity.py)")
+    with pytest.raises(sw.SwError) as ei:
+        sw.Database.load(path)
+    assert ei.value.code == (sw.SW_ECUDA if corrupt == "none" else sw.SW_EINVAL), sw.lib().sw_last_error()

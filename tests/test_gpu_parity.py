@@ -314,6 +314,28 @@ def test_persistent_index_roundtrip(tmp_path):
     assert np.array_equal(r1.scores, ref)
 
 
+def test_index_file_matches_layout_definition(tmp_path):
+    """f2: sw_db_save writes byte-for-byte the file tests/index_file.py builds from the layout's definition,
+    and a hand-written file loads and searches equal to the oracle."""
+    import index_file
+    rng = np.random.default_rng(92)
+    db = random_db(92, rng.integers(0, 400, size=700))
+    gids = rng.permutation(50_000)[:700].astype(np.int64)
+    crafted = str(tmp_path / "crafted.swb")
+    saved = str(tmp_path / "saved.swb")
+    index_file.write(crafted, index_file.build(db.residues, db.offsets, db.lengths, gids))
+    with sw.Database(db.residues, db.offsets, db.lengths, global_ids=gids, device=0) as g:
+        g.save(saved)
+    assert open(saved, "rb").read() == open(crafted, "rb").read()
+    q = _query(300, 92)
+    with sw.Database.load(crafted, device=0) as h:
+        r = h.search(q, B62, 2, 12, k=15)
+    ref = oracle.db_scores(q, db, B62, 2, 12)
+    assert np.array_equal(r.scores, ref)
+    ti, ts = oracle.topk(ref, 15, gids)
+    assert np.array_equal(r.topk_ids, ti) and np.array_equal(r.topk_scores, ts)
+
+
 @pytest.mark.parametrize("first_stage", [16, 8, 32])
 def test_very_long_subjects_exceeding_boundary_slab(first_stage):
     """Subjects longer than the per-warp boundary slab (6,144 columns): inter-task
