@@ -1,5 +1,5 @@
-"""bench.py host logic (no GPU): the analytic DRAM traffic model and the snake
-partition used for the multi-GPU shards."""
+"""bench.py host logic (no GPU): the analytic DRAM traffic model, the snake
+partition used for the multi-GPU shards, and the reference arm's JSON contract."""
 import numpy as np
 
 import bench
@@ -27,3 +27,28 @@ def test_snake_partition_covers_and_balances():
     assert np.array_equal(allids, np.arange(lens.size))
     tot = [int(lens[p].sum()) for p in parts]
     assert max(tot) - min(tot) <= 2 * int(lens.max())
+
+
+def test_reference_arm_contract_under_torchrun():
+    """`bench.py --impl reference` under torchrun (N=2): rank 0 alone prints ONE JSON line with the
+    contract's keys; every rank exits 0 (the oracle is the reference arm for this tier)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = 29500 + os.getpid() % 1000
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--impl", "reference",
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--config", "C1", "--ref-sample", "300"]
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["steps"] == 2 and d["warmup"] == 1
+    assert d["value"] > 0 and d["e2e"]["value"] == d["value"] and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
