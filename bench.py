@@ -322,17 +322,29 @@ def main():
             db.search(q, M, base.alpha, base.beta, k, scores=h_scores, topk_ids=h_ti, topk_scores=h_ts)
         if world > 1:
             dist.barrier()
+        def e2e_step():
+            db.search(q, M, base.alpha, base.beta, k, scores=h_scores, topk_ids=h_ti, topk_scores=h_ts)
+            if world > 1:   # the user-visible answer at N GPUs is the merged top-k (on rank 0)
+                d_ti.copy_(torch.from_numpy(h_ti))
+                d_ts.copy_(torch.from_numpy(h_ts))
+                dist.all_gather_into_tensor(g_ti, d_ti)
+                dist.all_gather_into_tensor(g_ts, d_ts)
+                if rank == 0:
+                    sw.merge_topk(g_ti.view(world, k).cpu().numpy(), g_ts.view(world, k).cpu().numpy(), k)
+
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            db.search(q, M, base.alpha, base.beta, k, scores=h_scores, topk_ids=h_ti, topk_scores=h_ts)
+            e2e_step()
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": round(cells_total / (dt / args.steps) / 1e9, 2), "unit": "GCUPS",
-               "h2d_bytes_per_step": int(q.size + 1024), "d2h_bytes_per_step": int(4 * n + 12 * k),
-               "api": "sw_search (blocking, pinned host buffers)"}
+               "h2d_bytes_per_step": int(q.size + 1024 + (12 * k if world > 1 else 0)),
+               "d2h_bytes_per_step": int(4 * n + 12 * k + (12 * k * world if world > 1 and rank == 0 else 0)),
+               "api": "sw_search (blocking, pinned host buffers)" +
+                      (" + top-k all-gather and sw_merge_topk on rank 0" if world > 1 else "")}
 
     if rank == 0:
         f_run = (clk.get("sm_mhz") or 1965.0) * 1e6
