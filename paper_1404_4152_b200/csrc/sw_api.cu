@@ -115,7 +115,24 @@ IntraShape intra_shape(int m_pad) {
   sh.smem = sh.bytes <= (size_t)kMaxSmemProfile;
   return sh;
 }
+template <int NC>
+void* intra_kernel_nc(const IntraShape& sh) {
+  switch (sh.tr) {
+    case 4: return sh.smem ? (void*)swk::k_intra16<4, true, NC> : (void*)swk::k_intra16<4, false, NC>;
+    case 5: return sh.smem ? (void*)swk::k_intra16<5, true, NC> : (void*)swk::k_intra16<5, false, NC>;
+    case 6: return sh.smem ? (void*)swk::k_intra16<6, true, NC> : (void*)swk::k_intra16<6, false, NC>;
+    case 7: return sh.smem ? (void*)swk::k_intra16<7, true, NC> : (void*)swk::k_intra16<7, false, NC>;
+    case 8: return sh.smem ? (void*)swk::k_intra16<8, true, NC> : (void*)swk::k_intra16<8, false, NC>;
+    case 10: return sh.smem ? (void*)swk::k_intra16<10, true, NC> : (void*)swk::k_intra16<10, false, NC>;
+    case 12: return sh.smem ? (void*)swk::k_intra16<12, true, NC> : (void*)swk::k_intra16<12, false, NC>;
+    case 14: return sh.smem ? (void*)swk::k_intra16<14, true, NC> : (void*)swk::k_intra16<14, false, NC>;
+    default: return sh.smem ? (void*)swk::k_intra16<16, true, NC> : (void*)swk::k_intra16<16, false, NC>;
+  }
+}
 void* intra_kernel(const IntraShape& sh) {
+  const char* e = getenv("SW_INTRA_NC");     // measurement switch: columns per wavefront step (default 4)
+  const int nc = e && atoi(e) == 2 ? 2 : 4;
+  if (nc == 4) return intra_kernel_nc<4>(sh);
   switch (sh.tr) {
     case 4: return sh.smem ? (void*)swk::k_intra16<4, true> : (void*)swk::k_intra16<4, false>;
     case 5: return sh.smem ? (void*)swk::k_intra16<5, true> : (void*)swk::k_intra16<5, false>;

@@ -367,6 +367,146 @@ __device__ __forceinline__ uint32_t intra_pair16(const uint2* __restrict__ pw, i
 }
 
 
+// NC columns per wavefront step (NC = 4: twice the work per step of
+// intra_pair16, so the per-step SHFL / profile-load / loop latency is paid once
+// per four columns).  Column c of step s on lane l is NC*k - 1 + c, k = s - l,
+// run with a c-row skew; D, F are shared in place as in col16b_x2.
+template <int R, int NC>
+__device__ __forceinline__ void col16b_xn(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t (&e)[NC],
+                                          uint32_t (&hp)[NC], const uint4 (&pa)[NC], const uint4 (&pb)[NC],
+                                          uint32_t na2, uint32_t nb2, uint32_t& hmax) {
+  uint32_t pend = 0u;
+  int npend = 0;
+#pragma unroll
+  for (int r = 0; r < R + NC - 1; r++) {
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      const int q = r - c;
+      if (q >= 0 && q < R) {
+        const uint32_t wa = q < 4 ? pa[c].x : q < 8 ? pa[c].y : q < 12 ? pa[c].z : pa[c].w;
+        const uint32_t wb = q < 4 ? pb[c].x : q < 8 ? pb[c].y : q < 12 ? pb[c].z : pb[c].w;
+        const uint32_t h = __vimax3_s16x2(D[q], e[c], F[q]);
+        D[q] = __vadd2(hp[c], prmt(wa, wb, sel_pair(q & 3)));   // H(i-1, col) + fsbt(q_i, s_{col+1})
+        const uint32_t hb = __vadd2(h, nb2);
+        e[c] = __viaddmax_s16x2_relu(e[c], na2, hb);
+        F[q] = __viaddmax_s16x2_relu(F[q], na2, hb);
+        hp[c] = h;
+        if (npend) hmax = __vimax3_s16x2(hmax, pend, h);
+        else pend = h;
+        npend ^= 1;
+      }
+    }
+  }
+  if (npend) hmax = __vmaxs2(hmax, pend);
+}
+
+template <int TR, bool SMEM, int NC>
+__device__ __forceinline__ uint32_t intra_multi16(const uint2* __restrict__ pw, int ncols,
+                                                  const int8_t* __restrict__ gprof, int stride, int m_pad,
+                                                  uint2* __restrict__ gbnd, long long gstride,
+                                                  uint32_t na2, uint32_t nb2, int lane) {
+  static_assert(NC == 2 || NC == 4, "columns per step");
+  constexpr int NR = NC / 2;                                              // residue words (4 codes each)
+  const int8_t* prof = prof_base<SMEM>(gprof);
+  uint32_t hmax = 0u;
+  const int nwords = (ncols + kResPerWord - 1) / kResPerWord;
+  const int K = (ncols + NC) / NC;                                        // steps of NC columns from -1
+  int pass = 0;
+  for (int base = 0; base < m_pad; base += 32 * TR, pass++) {
+    const int nact = min(32, (m_pad - base + TR - 1) / TR);
+    const bool first = base == 0, last = base + 32 * TR >= m_pad;
+    const uint2* gin = gbnd + (long long)(pass & 1) * gstride;
+    uint2* gout = gbnd + (long long)((pass + 1) & 1) * gstride;
+    const int8_t* pr = prof + (base / TR + lane) * 16;
+    uint32_t D[TR], F[TR];
+#pragma unroll
+    for (int r = 0; r < TR; r++) { D[r] = 0u; F[r] = 0u; }
+    uint32_t e_out[NC], h_out[NC], r_out[NR];
+#pragma unroll
+    for (int c = 0; c < NC; c++) { e_out[c] = 0u; h_out[c] = 0u; }
+#pragma unroll
+    for (int i = 0; i < NR; i++) r_out[i] = 0u;
+    // lane 0's inputs of step k (residues of columns NC*k .. NC*k+NC-1, and the
+    // previous pass's boundary of columns NC*k-1 ..), fetched 32 steps at a time
+    auto fetch = [&](int kb, uint32_t (&rp)[NR], uint2 (&g)[NC]) {
+      const int k = kb + lane;
+#pragma unroll
+      for (int i = 0; i < NR; i++) {
+        const int c0 = NC * k + 2 * i, c1 = c0 + 1;
+        const uint2 w0 = res_word(pw, c0, nwords), w1 = res_word(pw, c1, nwords);
+        const int s0 = res_shift(c0), s1 = res_shift(c1);
+        rp[i] = ((w0.x >> s0) & 31u) | (((w0.y >> s0) & 31u) << 5) | (((w1.x >> s1) & 31u) << 10) |
+                (((w1.y >> s1) & 31u) << 15);
+      }
+#pragma unroll
+      for (int c = 0; c < NC; c++) {
+        const int col = NC * k - 1 + c;
+        g[c] = (!first && col >= 0 && col < ncols) ? gin[col] : make_uint2(0u, 0u);
+      }
+    };
+    const int nsteps = K + nact - 1;
+    uint32_t rp_cur[NR], rp_nxt[NR];
+    uint2 g_cur[NC], g_nxt[NC];
+    fetch(0, rp_cur, g_cur);
+    fetch(32, rp_nxt, g_nxt);
+    __syncwarp();
+    for (int sb = 0; sb < nsteps; sb += 32) {
+#pragma unroll 1
+      for (int t = 0; t < 32; t++) {
+        const int s = sb + t;
+        if (s >= nsteps) break;
+        uint32_t e[NC], hp[NC], r_in[NR];
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+          e[c] = __shfl_up_sync(0xffffffffu, e_out[c], 1);
+          hp[c] = __shfl_up_sync(0xffffffffu, h_out[c], 1);
+        }
+#pragma unroll
+        for (int i = 0; i < NR; i++) r_in[i] = __shfl_up_sync(0xffffffffu, r_out[i], 1);
+#pragma unroll
+        for (int i = 0; i < NR; i++) {
+          const uint32_t v = __shfl_sync(0xffffffffu, rp_cur[i], t);
+          if (lane == 0) r_in[i] = v;
+        }
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+          const uint32_t gx = __shfl_sync(0xffffffffu, g_cur[c].x, t), gy = __shfl_sync(0xffffffffu, g_cur[c].y, t);
+          if (lane == 0) { e[c] = gx; hp[c] = gy; }                       // E(base, col), H(base-1, col)
+        }
+        const int k = s - lane;
+        if (lane < nact && k >= 0 && k < K) {
+          uint4 pa[NC], pb[NC];
+#pragma unroll
+          for (int c = 0; c < NC; c++) {
+            const uint32_t rr = r_in[c >> 1] >> (10 * (c & 1));
+            pa[c] = *reinterpret_cast<const uint4*>(pr + (rr & 31u) * stride);
+            pb[c] = *reinterpret_cast<const uint4*>(pr + ((rr >> 5) & 31u) * stride);
+          }
+          col16b_xn<TR, NC>(D, F, e, hp, pa, pb, na2, nb2, hmax);
+#pragma unroll
+          for (int c = 0; c < NC; c++) { e_out[c] = e[c]; h_out[c] = hp[c]; }
+#pragma unroll
+          for (int i = 0; i < NR; i++) r_out[i] = r_in[i];
+          if (!last && lane == nact - 1) {
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+              const int col = NC * k - 1 + c;
+              if (col >= 0 && col < ncols) gout[col] = make_uint2(e[c], hp[c]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NR; i++) rp_cur[i] = rp_nxt[i];
+#pragma unroll
+      for (int c = 0; c < NC; c++) g_cur[c] = g_nxt[c];
+      fetch(sb + 64, rp_nxt, g_nxt);
+    }
+    __syncwarp();
+  }
+  return hmax;
+}
+
 template <int T, bool SMEM, int NT, bool BIG = false, bool STATIC = false>
 __global__ void __launch_bounds__(NT, 1)
 k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
@@ -420,7 +560,7 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
 // Intra-task pass over groups [split, n_groups): one subject PAIR per work item,
 // longest first, aligned by the lane wavefront.  A kernel of its own (own
 // register allocation), launched on a second stream beside k_inter16.
-template <int TR, bool SMEM>
+template <int TR, bool SMEM, int NC = 2>
 __global__ void __launch_bounds__(kInterThreads, 1)
 k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
           const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
@@ -460,8 +600,13 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     const int p = 31 - item % 32;
     const GroupDesc gd = groups[g];
     if (2 * p >= gd.count) continue;
-    uint32_t hm = intra_pair16<TR, SMEM>(words + gd.base + p, gd.ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
-                                         na2, nb2, lane);
+    uint32_t hm;
+    if constexpr (NC == 2)
+      hm = intra_pair16<TR, SMEM>(words + gd.base + p, gd.ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
+                                  na2, nb2, lane);
+    else
+      hm = intra_multi16<TR, SMEM, NC>(words + gd.base + p, gd.ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
+                                       na2, nb2, lane);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) hm = __vmaxs2(hm, __shfl_xor_sync(0xffffffffu, hm, o));
     if (lane == 0) emit_pair(hm, g, 2 * p, gd.count, limit, pos_map, score_sorted, flag);

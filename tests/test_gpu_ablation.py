@@ -53,3 +53,28 @@ def test_variant_saturation(monkeypatch, variant, m):
         r = g.search(q, M, 2, 12, k=3)
     ref = oracle.db_scores(q, db, M, 2, 12)
     assert np.array_equal(r.scores, ref) and r.stats["n_rerun32"] >= 1
+
+
+@pytest.mark.parametrize("nc", ["2", "4"])
+@pytest.mark.parametrize("m", [1, 8, 129, 144, 300, 600, 1100])
+def test_intra_columns_per_step(monkeypatch, nc, m):
+    """The intra-task wavefront with 2 (previous design, SW_INTRA_NC=2) or 4 (default) columns per step,
+    every group forced through it: exact, across rows-per-lane shapes, multi-pass queries, ragged
+    column counts (every ncols mod 4) and int32 reruns of planted copies."""
+    monkeypatch.setenv("SW_INTRA_NC", nc)
+    monkeypatch.setenv("SW_LONG_COLS", "1")
+    rng = np.random.default_rng(50 + m)
+    lens = np.concatenate([rng.integers(0, 400, 300), [1, 2, 3, 4, 5, 2999, 3000, 3001, 3002]])
+    db = random_db(500 + m, lens)
+    q = _query(m, 5)
+    M = B62.copy()
+    if m >= 600:
+        for c in range(20):
+            M[c, c] = 60                                  # planted copies score > LIMIT16
+        db.residues[db.offsets[-1]:db.offsets[-1] + m] = q
+    for first_stage in (16, 32):
+        with sw.Database.from_synth(db, device=0, first_stage=first_stage) as g:
+            r = g.search(q, M, 2, 12, k=10)
+        ref = oracle.db_scores(q, db, M, 2, 12)
+        bad = np.nonzero(r.scores != ref)[0]
+        assert bad.size == 0, (nc, m, first_stage, bad[:5], r.scores[bad[:5]], ref[bad[:5]])
