@@ -559,14 +559,17 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
 
 // Intra-task pass over groups [split, n_groups): one subject PAIR per work item,
 // longest first, aligned by the lane wavefront.  A kernel of its own (own
-// register allocation), launched on a second stream beside k_inter16.
+// register allocation), launched beside k_inter16.
+// len_sorted (first pass only; NULL for rerun layouts): each pair runs to its own
+// longer subject's length instead of the group's ncols (the columns past it are
+// DUMMY padding, score-neutral).
 template <int TR, bool SMEM, int NC = 2>
 __global__ void __launch_bounds__(kInterThreads, 1)
 k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
           const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
-          int* __restrict__ score_sorted, uint8_t* __restrict__ flag) {
+          int* __restrict__ score_sorted, uint8_t* __restrict__ flag, const int* __restrict__ len_sorted) {
   // The inter-task kernel may start beside this one (programmatic dependent
   // launch): it only reads what was complete before this grid started.
   asm volatile("griddepcontrol.launch_dependents;");
@@ -600,12 +603,13 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     const int p = 31 - item % 32;
     const GroupDesc gd = groups[g];
     if (2 * p >= gd.count) continue;
+    const int ncols = len_sorted ? len_sorted[(long long)g * kGroup + min(2 * p + 1, gd.count - 1)] : gd.ncols;
     uint32_t hm;
     if constexpr (NC == 2)
-      hm = intra_pair16<TR, SMEM>(words + gd.base + p, gd.ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
+      hm = intra_pair16<TR, SMEM>(words + gd.base + p, ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
                                   na2, nb2, lane);
     else
-      hm = intra_multi16<TR, SMEM, NC>(words + gd.base + p, gd.ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
+      hm = intra_multi16<TR, SMEM, NC>(words + gd.base + p, ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
                                        na2, nb2, lane);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) hm = __vmaxs2(hm, __shfl_xor_sync(0xffffffffu, hm, o));
