@@ -93,7 +93,8 @@ def summarize_launches(path, prefix):
             continue
         name = d["Kernel Name"].split("(")[0][:80]
         val = float(d["Metric Value"].replace(",", ""))
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(d.get("Metric Unit", "nsecond"), 1.0)
+        unit = d.get("Metric Unit", "ns")
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1e-3)
         agg[name][0] += 1
         agg[name][1] += val * scale
         total += val * scale
