@@ -145,18 +145,36 @@ __global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* _
         if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
       }
       __syncthreads();
-      if (threadIdx.x == 0) {                                  // digit with (# > d) < kk <= (# >= d)
-        long long above = 0;
+      if (threadIdx.x < 32) {                                  // digit with (# > d) < kk <= (# >= d)
+        // warp 0: lane l owns digits 255-8l .. 248-8l (descending); exclusive
+        // scan of the lane sums gives the count above each lane's first digit
+        const int lane = threadIdx.x;
+        unsigned c[8];
+        unsigned sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          c[j] = hist[255 - 8 * lane - j];
+          sum += c[j];
+        }
+        unsigned incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
         const long long kk = sh_kk;
-        for (int d = 255; d >= 0; d--) {
-          const long long c = hist[d];
-          if (above < kk && kk <= above + c) {
-            sh_kk = kk - above;
-            sh_prefix = prefix | ((unsigned long long)d << shift);
-            sh_mask = mask | (255ull << shift);
-            break;
+        long long above = (long long)(incl - sum);
+        if (above < kk && kk <= above + (long long)sum) {      // exactly one lane
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            if (above < kk && kk <= above + (long long)c[j]) {
+              const int d = 255 - 8 * lane - j;
+              sh_kk = kk - above;
+              sh_prefix = prefix | ((unsigned long long)d << shift);
+              sh_mask = mask | (255ull << shift);
+            }
+            above += c[j];
           }
-          above += c;
         }
       }
       __syncthreads();
