@@ -2,16 +2,25 @@
 """bench.py — GCUPS of one-query Smith-Waterman database search on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2] [--first-stage 16]
+                    [--config C5] [--n-per-rank N] [--first-stage 16]
 
 A step is one pass of the whole hot path (query profile,
-inter-task int16x2 pass, int32 rerun of saturated subjects, scatter + exact
-top-k) over the workload of BASELINE.json configs[1] (C2: one query of length
-464 vs 1M synthetic sequences, BLOSUM62, alpha=2, beta=12, top-10).  With
-N > 1 (torchrun, one rank per GPU) every rank holds a 1M-sequence shard of an
-N x 1M database (weak scaling), partitioned by residue count (snake order over
-the length-sorted ids), and the per-rank top-k lists are merged through an
-NCCL all_gather inside the timed step.
+inter-task int16x2 pass beside the intra-task wavefront, int32 rerun of
+saturated subjects, scatter + exact top-k) over the workload BASELINE.json's
+metric is quoted on: C5 (configs[4], the "1/2/4/8 B200" scaling run and the
+largest config one GPU holds): one query of length 1000 vs 50M synthetic
+sequences, BLOSUM50, alpha=2, beta=12, top-100.  At N > 1 (torchrun, one rank
+per GPU) the SAME database is snake-sharded by residue count over the N ranks
+(strong scaling); every rank generates only its shard, and the
+per-rank top-k lists are exchanged by an NCCL all_gather inside the timed step
+and merged with sw_merge_topk (paper_1404_4152_b200.dist.ShardedSearch).
+--n-per-rank M switches to weak scaling (M sequences per rank).
+
+Parity gate (a run is valid only if every score matches the
+oracle): after timing, the scores of every subject are gathered on rank 0,
+hashed per 65,536-sequence block and compared with the stored oracle digest
+tests/golden/digests/<config>_m<m>.json (written by tools/make_digests.py from
+oracle/ only), and the merged top-k with the digest's exact top-k.
 
 `value` is device time with the database and query resident; `e2e` is the same
 metric through the blocking C-ABI call sw_search with host buffers (query and
@@ -22,6 +31,7 @@ bounded sample of the same workload on this host's cores.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -112,21 +122,50 @@ def snake_partition(lengths: np.ndarray, world: int, rank: int) -> np.ndarray:
 
 
 def build_workload(cfg_name: str, world: int, rank: int, n_per_rank: int | None):
+    """This rank's shard of the config (strong scaling: the same database split
+    N ways; weak: n_per_rank sequences per rank)."""
     from swdata import CONFIGS, make_db, make_query
     from swdata.synth import Config, db_lengths
     base = CONFIGS[cfg_name]
-    n_total = (n_per_rank or base.n_seqs) * world
-    cfg = Config(**{**base.__dict__, "n_seqs": n_total}) if n_total != base.n_seqs else base
-    lengths_kind = db_lengths(cfg)
-    ids = snake_partition(lengths_kind[0], world, rank) if world > 1 else None
-    db = make_db(cfg, ids=ids, lengths_kind=lengths_kind)
+    cfg = base if not n_per_rank else Config(**{**base.__dict__, "n_seqs": n_per_rank * world})
+    lk = db_lengths(cfg)
+    ids = snake_partition(lk[0], world, rank) if world > 1 else None
+    shard = make_db(cfg, ids=ids, lengths_kind=lk)
     q = make_query(base)
-    return base, cfg, db, q, int(lengths_kind[0].sum())
+    return base, cfg, shard, q, int(lk[0].astype(np.int64).sum())
 
 
-def workload_text(base, m: int, n_per_gpu: int) -> str:
-    return (f"{base.name} (BASELINE.json configs[1]): query {m} vs {n_per_gpu} synthetic seqs per GPU "
-            f"(lognormal mean 350, [10,5000]), BLOSUM62 alpha=2 beta=12, all scores + top-{base.k}")
+def workload_text(base, cfg, m: int, residues: int) -> str:
+    from swdata.synth import CONFIGS
+    idx = list(CONFIGS).index(base.name) if base.name in CONFIGS else -1
+    tail = ", 0.1% 5k-35k tail" if base.long_p else ""
+    plant = ", 5% planted near-copies" if base.plant_p else ""
+    return (f"{base.name} (BASELINE.json configs[{idx}]): query {m} vs {cfg.n_seqs:,} synthetic seqs "
+            f"({residues:,} residues; lognormal mean 350, [10,5000]{tail}{plant}), "
+            f"{base.matrix.upper()} alpha={base.alpha} beta={base.beta}, all scores + top-{base.k}")
+
+
+def digest_path(cfg_name: str, m: int) -> str:
+    return os.path.join(ROOT, "tests", "golden", "digests", f"{cfg_name}_m{m}.json")
+
+
+def parity_gate(full_scores: np.ndarray, ids, ts, cfg_name: str, m: int, n_total: int) -> dict:
+    """Every subject's score against the stored oracle digest (per 65,536-block
+    SHA-256) and the merged top-k against the digest's exact top-k."""
+    path = digest_path(cfg_name, m)
+    if not os.path.exists(path):
+        return {"checked": False, "why": f"no oracle digest {os.path.relpath(path, ROOT)}"}
+    rec = json.load(open(path))
+    if rec["n_seqs"] != n_total:
+        return {"checked": False, "why": f"digest is for {rec['n_seqs']} seqs, run has {n_total}"}
+    B = rec["block"]
+    bad = [i for i, b in enumerate(range(0, n_total, B))
+           if hashlib.sha256(full_scores[b:b + B].astype("<i4").tobytes()).hexdigest() != rec["block_sha256"][i]]
+    kk = min(len(rec["topk_ids"]), len(ids))
+    topk_ok = list(map(int, ids[:kk])) == rec["topk_ids"][:kk] and list(map(int, ts[:kk])) == rec["topk_scores"][:kk]
+    return {"checked": True, "blocks": len(rec["block_sha256"]), "blocks_ok": len(rec["block_sha256"]) - len(bad),
+            "first_bad_block": bad[0] if bad else None, "topk_ok": bool(topk_ok), "ok": not bad and bool(topk_ok),
+            "digest": os.path.relpath(path, ROOT)}
 
 
 def run_reference(args, rank, world):
@@ -135,34 +174,39 @@ def run_reference(args, rank, world):
         return
     import oracle
     from swdata import CONFIGS, make_db, make_query
+    from swdata.synth import db_lengths
     base = CONFIGS[args.config]
     q = make_query(base)
     M = base.matrix32()
     cores = oracle.default_threads()
     rng = np.random.default_rng(0)
     n_sample = args.ref_sample
+    lk = db_lengths(base)
+    total_res = int(lk[0].astype(np.int64).sum())
     steps = []
-    full = make_db(base)
     cells_per_step = []
     for s in range(args.warmup + args.steps):
-        idx = np.sort(rng.choice(full.n_seqs, size=n_sample, replace=False))
+        idx = np.sort(rng.choice(base.n_seqs, size=min(n_sample, base.n_seqs), replace=False))
+        sample = make_db(base, ids=idx, lengths_kind=lk)          # only the sampled subjects are generated
         t0 = time.perf_counter()
-        oracle.db_scores(q, full, M, base.alpha, base.beta, nthreads=cores, sample=idx)
+        oracle.db_scores(q, sample, M, base.alpha, base.beta, nthreads=cores)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             steps.append(dt)
-            cells_per_step.append(int(full.lengths[idx].sum()) * q.size)
+            cells_per_step.append(int(sample.lengths.astype(np.int64).sum()) * q.size)
     tot = sum(steps)
     gcups = sum(cells_per_step) / tot / 1e9
     line = {"metric": METRIC, "value": round(gcups, 4), "unit": "GCUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_text(base, q.size, base.n_seqs), "seqs_total": base.n_seqs * world,
-                       "residues_total": int(full.lengths.sum()) * world, "k": base.k},
+            "config": {"workload": workload_text(base, base, q.size, total_res), "seqs_total": base.n_seqs,
+                       "residues_total": total_res, "k": base.k},
             "cpu_baseline": {"value": round(gcups, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
-                             "sample": f"each step: {n_sample} random subjects of {base.name} (the oracle over "
-                                       f"all {base.n_seqs} would take ~{base.n_seqs / n_sample:.0f}x longer)"},
+                             "cpu": oracle.cpu_model(), "compile_flags": " ".join(oracle.CFLAGS),
+                             "sample": f"each step: {min(n_sample, base.n_seqs)} random subjects of {base.name} "
+                                       f"(the oracle over all {base.n_seqs} would take "
+                                       f"~{base.n_seqs / min(n_sample, base.n_seqs):.0f}x longer)"},
             "e2e": {"value": round(gcups, 4), "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -183,8 +227,9 @@ def cpu_baseline(base, q, db, seconds_target=12.0):
     t0 = time.perf_counter()
     oracle.db_scores(q, db, M, base.alpha, base.beta, nthreads=cores, sample=idx)
     dt = time.perf_counter() - t0
-    cells = int(db.lengths[idx].sum()) * q.size
+    cells = int(db.lengths[idx].astype(np.int64).sum()) * q.size
     return {"value": round(cells / dt / 1e9, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
+            "cpu": oracle.cpu_model(), "compile_flags": " ".join(oracle.CFLAGS),
             "sample": f"{n} random subjects of the rank-0 shard ({cells:.3e} cells, {dt:.1f} s)"}
 
 
@@ -207,10 +252,11 @@ def traffic_model(lengths, m: int, n_warps: int = SMS * 12, tile_rows: int = 48)
     return {"db_bytes": db_bytes, "boundary_bytes": bnd, "total": db_bytes + bnd}
 
 
-def load_ncu_traffic():
-    """DRAM bytes per k_inter16 launch from the newest committed ncu --set full summary."""
+def load_ncu_traffic(config: str = "C5"):
+    """DRAM bytes per k_inter16 launch from the newest committed ncu --set full
+    summary of this config (profiles/r*_ncu_inter16_<config>.json)."""
     import glob
-    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_inter16*.json")))
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_inter16_{config}.json")))
     try:
         with open(paths[-1]) as f:
             d = json.load(f)
@@ -223,15 +269,16 @@ def load_ncu_traffic():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--first-stage", type=int, default=16)
-    ap.add_argument("--n-per-rank", type=int, default=None)
-    ap.add_argument("--ref-sample", type=int, default=100000)
+    ap.add_argument("--n-per-rank", type=int, default=None, help="weak scaling: sequences per rank")
+    ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
 
     world = env_int("WORLD_SIZE", 1)
@@ -244,34 +291,27 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1404_4152_b200 as sw
+    from paper_1404_4152_b200.dist import ShardedSearch
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    base, cfg, sdb, q, total_res = build_workload(args.config, world, rank, args.n_per_rank)
+    t_gen = time.perf_counter()
+    base, cfg, shard, q, total_res = build_workload(args.config, world, rank, args.n_per_rank)
+    t_gen = time.perf_counter() - t_gen
     M = base.matrix32()
     k = base.k
     t_create = time.perf_counter()
-    db = sw.Database.from_synth(sdb, global_ids=sdb.global_ids if world > 1 else None, device=local,
-                                first_stage=args.first_stage)
+    ss = ShardedSearch(shard, k, device=local, db_kwargs={"first_stage": args.first_stage})
     t_create = time.perf_counter() - t_create
-    n = sdb.n_seqs
-    cells_local = int(sdb.lengths.sum()) * q.size
+    db = ss.db
+    n = shard.n_seqs
+    cells_local = int(shard.lengths.astype(np.int64).sum()) * q.size
     cells_total = total_res * q.size
-
     stream = torch.cuda.Stream()
-    d_scores = torch.empty(n, dtype=torch.int32, device="cuda")
-    d_ti = torch.empty(k, dtype=torch.int64, device="cuda")
-    d_ts = torch.empty(k, dtype=torch.int32, device="cuda")
-    g_ti = torch.empty(world * k, dtype=torch.int64, device="cuda")
-    g_ts = torch.empty(world * k, dtype=torch.int32, device="cuda")
 
     def step():
-        db.search_async(q, M, base.alpha, base.beta, k, d_scores, d_ti, d_ts, stream=stream)
-        if world > 1:
-            with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(g_ti, d_ti)
-                dist.all_gather_into_tensor(g_ts, d_ts)
+        ss.enqueue(q, M, base.alpha, base.beta, stream)
 
     for _ in range(args.warmup):
         step()
@@ -305,36 +345,35 @@ def main():
     ms_rerun = statistics.mean(s[2] for s in stage)
     ms_step = ms_total / args.steps
     gcups = cells_total / (ms_step * 1e-3) / 1e9
+    mi, ms = ss.merged_topk()
 
-    # merged top-k (host merge of the gathered lists; checked once, outside timing)
-    if world > 1:
-        mi, ms = sw.merge_topk(g_ti.view(world, k).cpu().numpy(), g_ts.view(world, k).cpu().numpy(), k)
-    else:
-        mi, ms = d_ti.cpu().numpy(), d_ts.cpu().numpy()
+    # ---- parity gate: every score on rank 0, against the stored oracle digest ----
+    parity = None
+    if not args.no_parity:
+        n_total = cfg.n_seqs
+        if world > 1:
+            full = torch.zeros(n_total, dtype=torch.int32, device="cuda")
+            gid = torch.from_numpy(shard.global_ids).cuda()
+            full[gid] = ss.d_scores[:n]
+            dist.reduce(full, dst=0, op=dist.ReduceOp.SUM)      # disjoint shards: a sum is a scatter
+            full_h = full.cpu().numpy() if rank == 0 else None
+            del full
+        else:
+            full_h = ss.d_scores[:n].cpu().numpy()
+        if rank == 0:
+            parity = parity_gate(full_h, mi, ms, args.config, q.size, n_total)
 
-    # ---- e2e: blocking C-ABI call with host buffers (H2D query+matrix, D2H scores + top-k) ----
+    # ---- e2e: blocking C-ABI call with host buffers (H2D query+matrix, D2H scores + top-k) + exchange ----
     e2e = None
     if not args.no_e2e:
-        h_scores = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
-        h_ti = torch.empty(k, dtype=torch.int64, pin_memory=True).numpy()
-        h_ts = torch.empty(k, dtype=torch.int32, pin_memory=True).numpy()
+        h_scores = torch.empty(max(n, 1), dtype=torch.int32, pin_memory=True).numpy()[:n]
         for _ in range(2):
-            db.search(q, M, base.alpha, base.beta, k, scores=h_scores, topk_ids=h_ti, topk_scores=h_ts)
+            ss.search(q, M, base.alpha, base.beta, scores=h_scores)
         if world > 1:
             dist.barrier()
-        def e2e_step():
-            db.search(q, M, base.alpha, base.beta, k, scores=h_scores, topk_ids=h_ti, topk_scores=h_ts)
-            if world > 1:   # the user-visible answer at N GPUs is the merged top-k (on rank 0)
-                d_ti.copy_(torch.from_numpy(h_ti))
-                d_ts.copy_(torch.from_numpy(h_ts))
-                dist.all_gather_into_tensor(g_ti, d_ti)
-                dist.all_gather_into_tensor(g_ts, d_ts)
-                if rank == 0:
-                    sw.merge_topk(g_ti.view(world, k).cpu().numpy(), g_ts.view(world, k).cpu().numpy(), k)
-
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            e2e_step()
+            ss.search(q, M, base.alpha, base.beta, scores=h_scores)
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], dtype=torch.float64, device="cuda")
@@ -342,9 +381,9 @@ def main():
             dt = float(t.item())
         e2e = {"value": round(cells_total / (dt / args.steps) / 1e9, 2), "unit": "GCUPS",
                "h2d_bytes_per_step": int(q.size + 1024 + (12 * k if world > 1 else 0)),
-               "d2h_bytes_per_step": int(4 * n + 12 * k + (12 * k * world if world > 1 and rank == 0 else 0)),
+               "d2h_bytes_per_step": int(4 * n + 12 * k + (12 * k * world if world > 1 else 0)),
                "api": "sw_search (blocking, pinned host buffers)" +
-                      (" + top-k all-gather and sw_merge_topk on rank 0" if world > 1 else "")}
+                      (" + top-k all_gather and sw_merge_topk" if world > 1 else "")}
 
     if rank == 0:
         f_run = (clk.get("sm_mhz") or 1965.0) * 1e6
@@ -354,24 +393,26 @@ def main():
         line = {
             "metric": METRIC, "value": round(gcups, 2), "unit": "GCUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int16x2+int32",
-            "data": "synthetic",
-            "config": {"workload": workload_text(base, q.size, n),
-                       "seqs_total": cfg.n_seqs, "residues_total": total_res, "cells_per_step": cells_total,
-                       "k": k, "first_stage": args.first_stage,
+            "higher_is_better": True, "scaling": "weak" if args.n_per_rank else "strong", "vs_baseline": None,
+            "dtype": "int16x2+int32", "data": "synthetic",
+            "config": {"workload": workload_text(base, cfg, q.size, total_res),
+                       "seqs_total": cfg.n_seqs, "seqs_rank0": n, "residues_total": total_res,
+                       "cells_per_step": cells_total, "k": k, "first_stage": args.first_stage,
                        "l2": "inputs larger than L2 (packed DB %.0f MB/GPU > 126 MB)" % (info1["packed_bytes"] / 1e6),
-                       "parallelism": f"dp{world} (residue-balanced shards)" if world > 1 else "1 GPU"},
+                       "parallelism": (f"{world} ranks, residue-balanced snake shards of one database, "
+                                       f"top-k all_gather (NCCL)") if world > 1 else "1 GPU"},
+            "parity": parity,
             "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_max, 1),
                          "unit": "Gcell/s", "frac": round(achieved / peak_max, 4),
                          "frac_at_run_clock": round(achieved / peak_run, 4),
                          # one PRMT per int16x2 row merges the two subjects' substitution scores
                          # (2.25 alu ops per cell): the kernel's own instruction-mix bound
                          "frac_of_mix_bound_2p25": round(achieved / (peak_max * ALU_OPS_PER_CELL / 2.25), 4),
-                         "kernel": "k_inter16 (int16x2 DPX first pass)",
+                         "kernel": "k_inter16 (int16x2 DPX first pass, beside k_intra16)",
                          "kernel_ms": round(ms_inter, 4), "kernel_share_of_step": round(ms_inter / ms_step, 4),
                          "peak_basis": "148 SM x 1965 MHz x 64 DPX lanes/clk/SM (measured) / 1.75 alu-pipe ops per cell",
-                         **load_ncu_traffic(),
-                         "traffic_model": {**traffic_model(sdb.lengths, q.size),
+                         **load_ncu_traffic(args.config),
+                         "traffic_model": {**traffic_model(shard.lengths, q.size),
                                            "note": "analytic: packed DB read once + DP boundary rows at "
                                                    "query-tile edges (DESIGN.md §5); the ncu traffic is "
                                                    "this, not re-reads of the input"}},
@@ -379,15 +420,16 @@ def main():
             "gpu_launches": int(launches),
             "e2e": e2e,
             "rerun_ms": round(ms_rerun, 4),
+            "gen_s": round(t_gen, 2),
             "db_create_s": round(t_create, 2),
             "topk_head": [int(x) for x in ms[:3]],
         }
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(base, q, sdb)
+            line["cpu_baseline"] = cpu_baseline(base, q, shard)
         elif not args.no_cpu_baseline:
             line["cpu_baseline"] = None
         print(json.dumps(line), flush=True)
-    db.close()
+    ss.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -63,6 +63,26 @@ extern "C" {
 
 typedef struct sw_db sw_db; /* opaque; owns its device memory */
 
+/*
+ * Measurement / test switches (SURVEY.md §8(f) f4 ablations and tile sweeps).
+ * Every field 0 = the production design.  They are read once, at
+ * sw_db_create / sw_db_load, never from the environment.  The production
+ * library libswsearch.so accepts only the defaults (SW_EINVAL otherwise); the
+ * ablation build libswsearch_ablation.so (same source, -DSW_ABLATION) carries
+ * the extra kernel instances.  Results never depend on any of them.
+ */
+typedef struct sw_tuning {
+  int32_t variant;        /* 0 production; 1 InterSP score profile, 2 IntraQP striped
+                             intra-task kernel, 3 static loop schedule (ablation build) */
+  int32_t tile_rows;      /* query rows per register tile of the int16x2 pass: 0 = 48; 32, 64 (ablation build) */
+  int32_t threads;        /* threads per persistent CTA: 0 = 384; 512 (ablation build) */
+  int32_t intra_cols;     /* columns per intra-task wavefront step: 0 = 4; 2 (ablation build) */
+  int32_t max_big;        /* inter-task groups wider than a warp's boundary slab that get a slab of
+                             their own: 0 = up to 2,048; > 0 at most this many; -1 none (tests) */
+  int32_t align_ws_kb;    /* sw_align direction workspace per batch in KiB: 0 = 1 GiB (tests force batching) */
+  int32_t reserved[2];    /* must be 0 */
+} sw_tuning;
+
 typedef struct sw_opts {
   int32_t device;         /* CUDA device ordinal; -1 = the caller's current device */
   int32_t first_stage;    /* lane width of the first pass: 8, 16 (default) or 32 */
@@ -79,7 +99,19 @@ typedef struct sw_opts {
                              HBM; first_stage 16 or 32; not with sw_search_batch) */
   int32_t chunk_mb;       /* residency 1: device bytes per streamed chunk in MiB
                              (two are allocated); 0 = 512 */
-  int32_t reserved[2];    /* must be 0 */
+  int32_t max_qlen;       /* per-search device buffers are allocated at create time for
+                             queries up to this length: 0 = 8192 (see sw_db_reserve) */
+  int32_t max_k;          /* ... and top-k up to this k: 0 = 4096 */
+  /* Device-memory hooks, e.g. torch's caching allocator.
+   * alloc(bytes, ctx) returns device memory on `device` (NULL = failure ->
+   * SW_ENOMEM); free(ptr, ctx) releases it.  Both NULL = cudaMalloc / cudaFree.
+   * Every device buffer of the handle comes from them; none is allocated by
+   * sw_search_async (buffers are sized at create time / by sw_db_reserve). */
+  void* (*alloc)(size_t bytes, void* ctx);
+  void (*free)(void* ptr, void* ctx);
+  void* alloc_ctx;
+  sw_tuning tuning;       /* measurement switches; zero = production */
+  int32_t reserved[4];    /* must be 0 */
 } sw_opts;
 
 typedef struct sw_stats {
@@ -104,15 +136,19 @@ typedef struct sw_db_info {
   int64_t scratch_bytes;        /* device bytes of DP boundary scratch */
   int64_t launches;             /* CUDA kernels launched by this handle so far */
   int64_t n_searches;           /* searches enqueued so far */
+  int64_t n_device_allocs;      /* device allocations made by this handle so far (alloc hook or cudaMalloc) */
+  int64_t device_bytes;         /* device bytes currently held by this handle */
   int32_t max_len;              /* longest subject */
   int32_t device;
   int32_t long_threshold;
   int32_t residency;            /* as sw_opts.residency */
   int32_t n_chunks;             /* residency 1: chunks streamed per search */
-  int32_t reserved[3];
+  int32_t max_qlen, max_k;      /* per-search buffer capacity (sw_opts.max_qlen / max_k, sw_db_reserve) */
+  int32_t reserved[1];
 } sw_db_info;
 
-/* Fill *opts with defaults (device -1, first_stage 16, long_threshold 0, residency 0). */
+/* Fill *opts with defaults (device -1, first_stage 16, long_threshold 0, residency 0,
+ * max_qlen 8192, max_k 4096, no allocator hooks, production tuning). */
 void sw_opts_default(sw_opts* opts);
 
 /*
@@ -123,8 +159,8 @@ void sw_opts_default(sw_opts* opts);
  *   residues   host, n_residues bytes, codes 0..23
  *   offsets    host, n_seqs int64: subject i = residues[offsets[i] .. +lengths[i])
  *   lengths    host, n_seqs int32 >= 0
- *   global_ids host, n_seqs int64 in [0, 2^32-2], or NULL (= 0..n_seqs-1); used
- *              only for top-k ids and the tie-break
+ *   global_ids host, n_seqs DISTINCT int64 in [0, 2^32-2], or NULL (= 0..n_seqs-1);
+ *              used only for top-k ids and the tie-break (a repeated id -> SW_EINVAL)
  *   opts       NULL = defaults
  *   out        receives the handle (NULL on error)
  */
@@ -163,6 +199,11 @@ int sw_search(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matri
  * stream) with DEVICE outputs and no host synchronisation.  query/matrix are
  * host pointers, staged by the library.  d_scores int32[n_seqs] (input order),
  * d_topk_ids int64[k], d_topk_scores int32[k]; any may be NULL.
+ * Never allocates and never blocks the host (except to recycle one of its
+ * eight pinned staging slots when eight searches are still in flight): qlen
+ * and k must fit the handle's capacity (sw_opts.max_qlen / max_k or
+ * sw_db_reserve), else SW_EINVAL before any device work.  Searches on one
+ * handle run in call order whatever streams they are enqueued on.
  */
 int sw_search_async(sw_db* db, const uint8_t* query, int32_t qlen, const int8_t* matrix,
                     int32_t alpha, int32_t beta, int32_t k, int32_t* d_scores,
@@ -238,6 +279,14 @@ int sw_encode(const char* text, int64_t n, uint8_t* out);
  */
 int sw_merge_topk(const int64_t* ids, const int32_t* scores, int32_t n_lists, int32_t k_in,
                   int32_t k_out, int64_t* out_ids, int32_t* out_scores);
+
+/*
+ * Grow the per-search device buffers for queries up to max_qlen residues and
+ * top-k up to max_k (never shrinks; blocks until the handle is idle).  The
+ * blocking calls (sw_search, sw_search_batch, sw_align) grow them on demand;
+ * sw_search_async needs them sized beforehand.
+ */
+int sw_db_reserve(sw_db* db, int32_t max_qlen, int32_t max_k);
 
 int sw_db_get_info(const sw_db* db, sw_db_info* info);
 

@@ -24,24 +24,46 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "_liboracle.so")
 _SRC = os.path.join(_HERE, "sw_oracle.c")
 _lib = None
 
-CFLAGS = ["-O2", "-shared", "-fPIC", "-pthread"]
+# BASELINE.md's CPU-baseline plan: plain scalar C, -O3 -march=native, no
+# intrinsics, flags recorded.  -march=native ties the binary to the host CPU,
+# so the library is built per CPU model (the GPU box builds its own on first use).
+CFLAGS = ["-O3", "-march=native", "-shared", "-fPIC", "-pthread"]
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _so_path() -> str:
+    import hashlib
+    tag = hashlib.sha1((cpu_model() + " ".join(CFLAGS)).encode()).hexdigest()[:10]
+    return os.path.join(_HERE, f"_liboracle_{tag}.so")
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", _SO, _SRC])
-    return _SO
+    so = _so_path()
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(_SRC):
+        tmp = f"{so}.{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC])
+        os.replace(tmp, so)
+    return so
 
 
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(_SO)
+        L = ctypes.CDLL(build())
         P = ctypes.c_void_p
         i32, i64 = ctypes.c_int32, ctypes.c_int64
         L.oracle_sw_score.argtypes = [P, i32, P, i32, P, i32, i32]

@@ -19,6 +19,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libswsearch.so")
+# Same source built with -DSW_ABLATION: the f4 ablation kernels and the
+# tile/CTA-size instances selected by sw_tuning (measurement only).
+ABLATION_LIB_PATH = os.path.join(_HERE, "libswsearch_ablation.so")
 
 SW_OK, SW_EINVAL, SW_ENOMEM, SW_ECUDA, SW_ERANGE, SW_EINTERNAL = 0, -1, -2, -3, -4, -5
 
@@ -29,11 +32,26 @@ class SwError(RuntimeError):
         self.code = code
 
 
+class sw_tuning(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int32), ("tile_rows", ctypes.c_int32), ("threads", ctypes.c_int32),
+                ("intra_cols", ctypes.c_int32), ("max_big", ctypes.c_int32), ("align_ws_kb", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
+
+
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class sw_opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("first_stage", ctypes.c_int32),
                 ("long_threshold", ctypes.c_int32), ("verbose", ctypes.c_int32),
                 ("residency", ctypes.c_int32), ("chunk_mb", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("max_qlen", ctypes.c_int32), ("max_k", ctypes.c_int32),
+                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
+                ("tuning", sw_tuning), ("reserved", ctypes.c_int32 * 4)]
+
+# variant names of sw_tuning.variant (f4 ablations)
+VARIANTS = {"production": 0, "intersp": 1, "intraqp": 2, "static": 3}
 
 
 class sw_stats(ctypes.Structure):
@@ -52,9 +70,10 @@ class sw_db_info(ctypes.Structure):
     _fields_ = [("n_seqs", ctypes.c_int64), ("n_residues", ctypes.c_int64), ("n_inter", ctypes.c_int64),
                 ("n_intra", ctypes.c_int64), ("n_groups", ctypes.c_int64), ("packed_bytes", ctypes.c_int64),
                 ("scratch_bytes", ctypes.c_int64), ("launches", ctypes.c_int64), ("n_searches", ctypes.c_int64),
+                ("n_device_allocs", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
                 ("max_len", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("long_threshold", ctypes.c_int32), ("residency", ctypes.c_int32), ("n_chunks", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("max_qlen", ctypes.c_int32), ("max_k", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class sw_alignment(ctypes.Structure):
@@ -65,19 +84,20 @@ class sw_alignment(ctypes.Structure):
 
 # Every symbol include/swsearch.h declares (tests check the .so exports all of them).
 EXPORTS = ("sw_opts_default", "sw_db_create", "sw_search", "sw_search_async", "sw_search_batch", "sw_merge_topk",
-           "sw_db_get_info", "sw_db_stage_times", "sw_align", "sw_encode", "sw_db_save", "sw_db_load", "sw_db_destroy", "sw_strerror",
-           "sw_last_error")
+           "sw_db_get_info", "sw_db_stage_times", "sw_db_reserve", "sw_align", "sw_encode", "sw_db_save",
+           "sw_db_load", "sw_db_destroy", "sw_strerror", "sw_last_error")
 
-_lib = None
+_libs = {}
 
 
-def lib() -> ctypes.CDLL:
-    """Load libswsearch.so; raises (no fallback) when it has not been built."""
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
-        L = ctypes.CDLL(LIB_PATH)
+def lib(ablation: bool = False) -> ctypes.CDLL:
+    """Load libswsearch.so (or the ablation build); raises (no fallback) when
+    it has not been built."""
+    path = ABLATION_LIB_PATH if ablation else LIB_PATH
+    if path not in _libs:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(path)
         P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         L.sw_opts_default.argtypes = [ctypes.POINTER(sw_opts)]
         L.sw_opts_default.restype = None
@@ -99,6 +119,8 @@ def lib() -> ctypes.CDLL:
         L.sw_db_get_info.restype = ctypes.c_int
         L.sw_db_stage_times.argtypes = [P, i32, ctypes.POINTER(ctypes.c_float)]
         L.sw_db_stage_times.restype = ctypes.c_int
+        L.sw_db_reserve.argtypes = [P, i32, i32]
+        L.sw_db_reserve.restype = ctypes.c_int
         L.sw_db_save.argtypes = [P, ctypes.c_char_p]
         L.sw_db_save.restype = ctypes.c_int
         L.sw_db_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(sw_opts), ctypes.POINTER(P)]
@@ -109,14 +131,73 @@ def lib() -> ctypes.CDLL:
         L.sw_strerror.restype = ctypes.c_char_p
         L.sw_last_error.argtypes = []
         L.sw_last_error.restype = ctypes.c_char_p
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
-def _check(rc: int):
+def _check(rc: int, L=None):
     if rc != SW_OK:
-        L = lib()
+        L = L or lib()
         raise SwError(rc, f"{L.sw_strerror(rc).decode()}: {L.sw_last_error().decode()}")
+
+
+class TorchAllocator:
+    """sw_opts.alloc / free backed by torch's CUDA caching allocator (SURVEY.md
+    §8(b)): the library's device buffers then come from torch's pool.  Counts
+    the calls (tests check that searches allocate nothing)."""
+
+    def __init__(self, device: int):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.n_alloc = 0
+        self.n_free = 0
+        self.live = {}
+
+        def _alloc(nbytes, ctx):
+            try:
+                ptr = torch.cuda.caching_allocator_alloc(int(nbytes), device=self.device)
+            except Exception:
+                return None
+            self.n_alloc += 1
+            self.live[int(ptr)] = int(nbytes)
+            return int(ptr)
+
+        def _free(ptr, ctx):
+            if ptr:
+                self.n_free += 1
+                self.live.pop(int(ptr), None)
+                torch.cuda.caching_allocator_delete(int(ptr))
+
+        self.alloc_fn = ALLOC_FN(_alloc)     # kept alive with the Database
+        self.free_fn = FREE_FN(_free)
+
+
+def _make_opts(L, device, first_stage, long_threshold, residency, chunk_mb, max_qlen, max_k, allocator,
+               tuning) -> sw_opts:
+    o = sw_opts()
+    L.sw_opts_default(ctypes.byref(o))
+    o.device, o.first_stage, o.long_threshold = device, first_stage, long_threshold
+    o.residency, o.chunk_mb = residency, chunk_mb
+    if max_qlen:
+        o.max_qlen = max_qlen
+    if max_k:
+        o.max_k = max_k
+    if allocator is not None:
+        o.alloc, o.free = allocator.alloc_fn, allocator.free_fn
+    for key, val in (tuning or {}).items():
+        if key == "variant" and isinstance(val, str):
+            val = VARIANTS[val]
+        setattr(o.tuning, key, int(val))
+    return o
+
+
+def _needs_ablation(tuning) -> bool:
+    t = tuning or {}
+    v = t.get("variant", 0)
+    v = VARIANTS[v] if isinstance(v, str) else v
+    return bool(v) or t.get("tile_rows", 0) not in (0, 48) or t.get("threads", 0) not in (0, 384) \
+        or t.get("intra_cols", 0) == 2
 
 
 def _ptr(a) -> int | None:
@@ -139,25 +220,40 @@ class Database:
     """sw_db_create / sw_db_destroy.  Arrays are copied (and packed) by the library."""
 
     def __init__(self, residues, offsets, lengths, global_ids=None, device: int = -1,
-                 first_stage: int = 16, long_threshold: int = 0, residency: int = 0, chunk_mb: int = 0):
-        L = lib()
+                 first_stage: int = 16, long_threshold: int = 0, residency: int = 0, chunk_mb: int = 0,
+                 max_qlen: int = 0, max_k: int = 0, allocator=None, tuning: dict | None = None):
+        """allocator: None (cudaMalloc), "torch" (torch's caching allocator) or a
+        TorchAllocator-like object with alloc_fn / free_fn ctypes callbacks.
+        tuning: sw_tuning fields (measurement switches; the non-production ones
+        load the ablation build)."""
+        L = lib(_needs_ablation(tuning))
         res = np.ascontiguousarray(residues, dtype=np.uint8)
         offs = np.ascontiguousarray(offsets, dtype=np.int64)
         lens = np.ascontiguousarray(lengths, dtype=np.int32)
         gids = None if global_ids is None else np.ascontiguousarray(global_ids, dtype=np.int64)
         if offs.shape != lens.shape:
             raise ValueError("offsets and lengths must have the same shape")
-        o = sw_opts()
-        L.sw_opts_default(ctypes.byref(o))
-        o.device, o.first_stage, o.long_threshold = device, first_stage, long_threshold
-        o.residency, o.chunk_mb = residency, chunk_mb
+        if allocator == "torch":
+            import torch
+            allocator = TorchAllocator(device if device >= 0 else torch.cuda.current_device())
+        o = _make_opts(L, device, first_stage, long_threshold, residency, chunk_mb, max_qlen, max_k, allocator,
+                       tuning)
         h = ctypes.c_void_p()
         _check(L.sw_db_create(_ptr(res) if res.size else None, res.size, _ptr(offs) if offs.size else None,
                               _ptr(lens) if lens.size else None, lens.size,
-                              None if gids is None else _ptr(gids), ctypes.byref(o), ctypes.byref(h)))
+                              None if gids is None else _ptr(gids), ctypes.byref(o), ctypes.byref(h)), L)
+        self._L = L
         self._h = h
+        self.allocator = allocator          # the callbacks must outlive the handle
         self.n_seqs = int(lens.size)
         self._lengths = lens.copy()        # sizes the ops buffer of align()
+
+    def _call(self, name, *args):
+        _check(getattr(self._L, name)(*args), self._L)
+
+    def reserve(self, max_qlen: int, max_k: int):
+        """sw_db_reserve: size the per-search buffers (sw_search_async never allocates)."""
+        self._call("sw_db_reserve", self._h, max_qlen, max_k)
 
     @classmethod
     def from_synth(cls, db, **kw) -> "Database":
@@ -165,34 +261,38 @@ class Database:
 
     @classmethod
     def load(cls, path: str, device: int = -1, first_stage: int = 16, long_threshold: int = 0,
-             residency: int = 0, chunk_mb: int = 0) -> "Database":
+             residency: int = 0, chunk_mb: int = 0, max_qlen: int = 0, max_k: int = 0, allocator=None,
+             tuning: dict | None = None) -> "Database":
         """sw_db_load: map a file written by save() and upload it (no re-sort / re-pack)."""
-        L = lib()
-        o = sw_opts()
-        L.sw_opts_default(ctypes.byref(o))
-        o.device, o.first_stage, o.long_threshold = device, first_stage, long_threshold
-        o.residency, o.chunk_mb = residency, chunk_mb
+        L = lib(_needs_ablation(tuning))
+        if allocator == "torch":
+            import torch
+            allocator = TorchAllocator(device if device >= 0 else torch.cuda.current_device())
+        o = _make_opts(L, device, first_stage, long_threshold, residency, chunk_mb, max_qlen, max_k, allocator,
+                       tuning)
         h = ctypes.c_void_p()
-        _check(L.sw_db_load(os.fsencode(path), ctypes.byref(o), ctypes.byref(h)))
+        _check(L.sw_db_load(os.fsencode(path), ctypes.byref(o), ctypes.byref(h)), L)
         self = cls.__new__(cls)
+        self._L = L
         self._h = h
+        self.allocator = allocator
         self._lengths = None
         self.n_seqs = self.info()["n_seqs"]
         return self
 
     def save(self, path: str):
         """sw_db_save: write the packed, length-sorted layout to `path`."""
-        _check(lib().sw_db_save(self._h, os.fsencode(path)))
+        self._call("sw_db_save", self._h, os.fsencode(path))
 
     def info(self) -> dict:
         i = sw_db_info()
-        _check(lib().sw_db_get_info(self._h, ctypes.byref(i)))
+        self._call("sw_db_get_info", self._h, ctypes.byref(i))
         return {f: getattr(i, f) for f, _ in i._fields_ if f != "reserved"}
 
     def stage_times(self, back: int = 1) -> list:
         """[profile, first pass, rerun, ranking] device ms of the search `back` calls ago."""
         ms = (ctypes.c_float * 4)()
-        _check(lib().sw_db_stage_times(self._h, back, ms))
+        self._call("sw_db_stage_times", self._h, back, ms)
         return list(ms)
 
     def search(self, query, matrix, alpha: int, beta: int, k: int = 10, scores: bool | np.ndarray = True,
@@ -212,8 +312,8 @@ class Database:
         ti = np.empty(k, dtype=np.int64) if topk_ids is None else topk_ids
         ts = np.empty(k, dtype=np.int32) if topk_scores is None else topk_scores
         st = sw_stats()
-        _check(lib().sw_search(self._h, _ptr(q), q.size, _ptr(M), alpha, beta, k, _ptr(sc), _ptr(ti),
-                               _ptr(ts), ctypes.byref(st)))
+        self._call("sw_search", self._h, _ptr(q), q.size, _ptr(M), alpha, beta, k, _ptr(sc), _ptr(ti),
+                               _ptr(ts), ctypes.byref(st))
         return SearchResult(sc, ti, ts, st.as_dict())
 
     def search_batch(self, queries, matrix, alpha: int, beta: int, k: int = 10, scores: bool = True):
@@ -230,8 +330,8 @@ class Database:
         ti = np.empty((len(qs), k), dtype=np.int64)
         ts = np.empty((len(qs), k), dtype=np.int32)
         st = sw_stats()
-        _check(lib().sw_search_batch(self._h, _ptr(cat) if cat.size else None, _ptr(offs), _ptr(lens), len(qs),
-                                     _ptr(M), alpha, beta, k, _ptr(sc), _ptr(ti), _ptr(ts), ctypes.byref(st)))
+        self._call("sw_search_batch", self._h, _ptr(cat) if cat.size else None, _ptr(offs), _ptr(lens), len(qs),
+                                     _ptr(M), alpha, beta, k, _ptr(sc), _ptr(ti), _ptr(ts), ctypes.byref(st))
         d = st.as_dict()
         d["pairs"] = st.reserved[0]
         return SearchResult(sc, ti, ts, d)
@@ -252,7 +352,7 @@ class Database:
         cap = int(n * q.size + (lens.sum() if lens is not None else n * (self.info()["max_len"])))
         out = (sw_alignment * n)()
         buf = ctypes.create_string_buffer(max(cap, 1))
-        _check(lib().sw_align(self._h, _ptr(q), q.size, _ptr(M), alpha, beta, _ptr(idx), n, out, buf, cap))
+        self._call("sw_align", self._h, _ptr(q), q.size, _ptr(M), alpha, beta, _ptr(idx), n, out, buf, cap)
         raw = buf.raw
         res = []
         for a in out:
@@ -273,12 +373,12 @@ class Database:
             h = stream.cuda_stream
         else:
             h = int(stream)
-        _check(lib().sw_search_async(self._h, _ptr(q), q.size, _ptr(M), alpha, beta, k, _ptr(d_scores),
-                                     _ptr(d_topk_ids), _ptr(d_topk_scores), h))
+        self._call("sw_search_async", self._h, _ptr(q), q.size, _ptr(M), alpha, beta, k, _ptr(d_scores),
+                                     _ptr(d_topk_ids), _ptr(d_topk_scores), h)
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().sw_db_destroy(self._h)
+            self._L.sw_db_destroy(self._h)
             self._h = None
 
     def __del__(self):

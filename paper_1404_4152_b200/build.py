@@ -13,19 +13,28 @@ SOURCES = [os.path.join(PKG, "csrc", "sw_api.cu")]
 DEPS = SOURCES + [os.path.join(PKG, "csrc", f) for f in sorted(os.listdir(os.path.join(PKG, "csrc")))
                   if f.endswith((".cuh", ".inc"))] + [os.path.join(ROOT, "include", "swsearch.h")]
 OUT = os.path.join(PKG, "libswsearch.so")
+# Same source with the f4 ablation kernels and tile/CTA-size instances
+# (sw_tuning); the production library above carries only the shipped design.
+OUT_ABLATION = os.path.join(PKG, "libswsearch_ablation.so")
 
 
 def _stale(out, deps):
     return not os.path.exists(out) or any(os.path.getmtime(d) > os.path.getmtime(out) for d in deps)
 
 
-def build_cuda(force=False, verbose=False):
-    if force or _stale(OUT, DEPS):
-        cmd = [NVCC, *ARCH, *NVFLAGS, "-shared", "-o", OUT, *SOURCES]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-            print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+def build_cuda(force=False, verbose=False, ablation=True):
+    jobs = []
+    targets = [(OUT, [])] + ([(OUT_ABLATION, ["-DSW_ABLATION"])] if ablation else [])
+    for out, extra in targets:
+        if force or _stale(out, DEPS):
+            cmd = [NVCC, *ARCH, *NVFLAGS, *extra, "-shared", "-o", out, *SOURCES]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+                print(" ".join(cmd), file=sys.stderr)
+            jobs.append((cmd, subprocess.Popen(cmd)))
+    for cmd, p in jobs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
     return OUT
 
 

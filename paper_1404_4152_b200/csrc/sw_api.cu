@@ -25,12 +25,14 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <nvtx3/nvToolsExt.h>
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -39,7 +41,9 @@
 #include "../../include/swsearch.h"
 #include "sw_kernels.cuh"
 #include "sw_align.cuh"
-#include "sw_ablation.cuh"
+#ifdef SW_ABLATION
+#include "sw_ablation.cuh"   // f4 kernels: only in the ablation build (libswsearch_ablation.so)
+#endif
 
 using swk::GroupDesc;
 
@@ -65,34 +69,76 @@ int fail(int code, const char* fmt, ...) {
                   #call, cudaGetErrorString(_e), __FILE__, __LINE__);                     \
   } while (0)
 
-constexpr int kTileRows = 48;        // default query rows per register tile (SW_TILE_ROWS overrides: 32/48/64)
+constexpr int kTileRows = 48;        // query rows per register tile (sw_tuning.tile_rows: 32/64 in the ablation build)
 
-int tile_rows_env() {
-  const char* e = getenv("SW_TILE_ROWS");
-  const int v = e ? atoi(e) : kTileRows;
-  return (v == 32 || v == 48 || v == 64) ? v : kTileRows;
-}
+#ifdef SW_ABLATION
+constexpr bool kAblationBuild = true;
+#else
+constexpr bool kAblationBuild = false;
+#endif
 
-int threads_env(int def) {
-  const char* e = getenv("SW_THREADS");
-  const int v = e ? atoi(e) : def;
-  return (v == 384 || v == 512) ? v : def;
+// NVTX range for the host side of a stage (enqueue / wait); header-only nvtx3.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-(device, kernel)
+// attribute shared by every handle in the process.  It is only ever RAISED,
+// under a process-wide lock, so a concurrent launch on another handle never
+// sees it drop below what that launch was set up for.
+int raise_smem_limit(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void*>, size_t>> set;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(SW_ECUDA, "cudaGetDevice failed");
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : set)
+    if (e.first.first == dev && e.first.second == fn) {
+      if (e.second >= bytes) return SW_OK;
+      cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (r != cudaSuccess) return fail(SW_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(r));
+      e.second = bytes;
+      return SW_OK;
+    }
+  cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(bytes, 1));
+  if (r != cudaSuccess) return fail(SW_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(r));
+  set.push_back({{dev, fn}, bytes});
+  return SW_OK;
 }
+#define CK_SMEM(fn, bytes)                                      \
+  do {                                                          \
+    int _rc = raise_smem_limit((const void*)(fn), (bytes));     \
+    if (_rc != SW_OK) return _rc;                               \
+  } while (0)
 
 template <int T, int NT>
 void* inter16_kernel(bool smem, bool big) {
   if (big) return smem ? (void*)swk::k_inter16<T, true, NT, true> : (void*)swk::k_inter16<T, false, NT, true>;
   return smem ? (void*)swk::k_inter16<T, true, NT> : (void*)swk::k_inter16<T, false, NT>;
 }
-// f4 ablation (SW_VARIANT=static): the paper's static loop schedule instead of the work queue
+#ifdef SW_ABLATION
+// f4 ablation (sw_tuning.variant 3): the paper's static loop schedule instead of the work queue
 inline void* inter16_kernel_static(bool smem, bool big) {
   if (big) return smem ? (void*)swk::k_inter16<48, true, 384, true, true> : (void*)swk::k_inter16<48, false, 384, true, true>;
   return smem ? (void*)swk::k_inter16<48, true, 384, false, true> : (void*)swk::k_inter16<48, false, 384, false, true>;
 }
+#endif
 
-template <int T>
-void* inter16_kernel_nt(bool smem, int nt, bool big) {
-  return nt == 512 ? inter16_kernel<T, 512>(smem, big) : inter16_kernel<T, 384>(smem, big);
+// The int16x2 first-pass instance for a tile height / CTA size (only 48 / 384
+// in the production build; sw_db_create rejects the others there).
+inline void* inter16_select(int T, int nt, bool smem, bool big, bool static_schedule) {
+#ifdef SW_ABLATION
+  if (static_schedule) return inter16_kernel_static(smem, big);
+  if (T == 32) return nt == 512 ? inter16_kernel<32, 512>(smem, big) : inter16_kernel<32, 384>(smem, big);
+  if (T == 64) return nt == 512 ? inter16_kernel<64, 512>(smem, big) : inter16_kernel<64, 384>(smem, big);
+  if (nt == 512) return inter16_kernel<48, 512>(smem, big);
+#else
+  (void)T;
+  (void)nt;
+  (void)static_schedule;
+#endif
+  return inter16_kernel<48, 384>(smem, big);
 }
 constexpr int kMaxSmemProfile = 200 * 1024;
 
@@ -117,6 +163,7 @@ IntraShape intra_shape(int m_pad) {
 }
 template <int NC>
 void* intra_kernel_nc(const IntraShape& sh) {
+  static_assert(NC == 2 || NC == 4, "columns per step");
   switch (sh.tr) {
     case 4: return sh.smem ? (void*)swk::k_intra16<4, true, NC> : (void*)swk::k_intra16<4, false, NC>;
     case 5: return sh.smem ? (void*)swk::k_intra16<5, true, NC> : (void*)swk::k_intra16<5, false, NC>;
@@ -129,21 +176,15 @@ void* intra_kernel_nc(const IntraShape& sh) {
     default: return sh.smem ? (void*)swk::k_intra16<16, true, NC> : (void*)swk::k_intra16<16, false, NC>;
   }
 }
-void* intra_kernel(const IntraShape& sh) {
-  const char* e = getenv("SW_INTRA_NC");     // measurement switch: columns per wavefront step (default 4)
-  const int nc = e && atoi(e) == 2 ? 2 : 4;
-  if (nc == 4) return intra_kernel_nc<4>(sh);
-  switch (sh.tr) {
-    case 4: return sh.smem ? (void*)swk::k_intra16<4, true> : (void*)swk::k_intra16<4, false>;
-    case 5: return sh.smem ? (void*)swk::k_intra16<5, true> : (void*)swk::k_intra16<5, false>;
-    case 6: return sh.smem ? (void*)swk::k_intra16<6, true> : (void*)swk::k_intra16<6, false>;
-    case 7: return sh.smem ? (void*)swk::k_intra16<7, true> : (void*)swk::k_intra16<7, false>;
-    case 8: return sh.smem ? (void*)swk::k_intra16<8, true> : (void*)swk::k_intra16<8, false>;
-    case 10: return sh.smem ? (void*)swk::k_intra16<10, true> : (void*)swk::k_intra16<10, false>;
-    case 12: return sh.smem ? (void*)swk::k_intra16<12, true> : (void*)swk::k_intra16<12, false>;
-    case 14: return sh.smem ? (void*)swk::k_intra16<14, true> : (void*)swk::k_intra16<14, false>;
-    default: return sh.smem ? (void*)swk::k_intra16<16, true> : (void*)swk::k_intra16<16, false>;
-  }
+// intra_cols: columns per wavefront step (4 = production; 2 = the previous
+// design, ablation build only)
+void* intra_kernel(const IntraShape& sh, int intra_cols) {
+#ifdef SW_ABLATION
+  if (intra_cols == 2) return intra_kernel_nc<2>(sh);
+#else
+  (void)intra_cols;
+#endif
+  return intra_kernel_nc<4>(sh);
 }
 
 int host_threads() {
@@ -175,6 +216,21 @@ struct sw_db {
   std::mutex mu;
   int first_stage = 16;
   int long_threshold = -1;
+  sw_tuning tuning = {};          // measurement switches, fixed at create / load
+
+  // device memory: the caller's hooks (sw_opts.alloc / free) or cudaMalloc / cudaFree
+  void* (*alloc_fn)(size_t, void*) = nullptr;
+  void (*free_fn)(void*, void*) = nullptr;
+  void* alloc_ctx = nullptr;
+  int64_t n_device_allocs = 0, device_bytes = 0;
+  std::vector<std::pair<void*, size_t>> live;   // every live device buffer (size for the byte count)
+
+  // capacity of the per-search buffers (sw_opts.max_qlen / max_k, sw_db_reserve)
+  int cap_qlen = 0, cap_k = 0;
+  // inter/intra split and wide-group slabs: a property of the layout, planned at create
+  int split_cut = 0;              // groups with ncols > split_cut go intra-task (pair by pair)
+  int n_big = 0;                  // inter-task groups wider than a warp slab with a slab of their own
+  long long big_cols = 0;         // columns per big slab
 
   int64_t n_seqs = 0, n_residues = 0, n_inter = 0, n_intra = 0, sum_len = 0;
   int32_t max_len = 0, max_inter_len = 0;
@@ -217,7 +273,7 @@ struct sw_db {
 
   // per-search buffers
   uint8_t* d_query = nullptr;
-  int query_cap = 0;
+  size_t query_cap = 0;
   int8_t* d_matrix = nullptr;
   int8_t* d_prof = nullptr;
   size_t prof_cap = 0;
@@ -226,7 +282,7 @@ struct sw_db {
   unsigned long long* d_keys = nullptr;
   unsigned long long* d_cand = nullptr;
   unsigned long long* d_cand2 = nullptr;
-  int cand_cap = 0;
+  size_t cand_cap = 0, cand2_cap = 0;   // bytes
   uint8_t* d_flag8 = nullptr;     // per sorted position: saturated in the int8 pass
   uint8_t* d_flag16 = nullptr;    // per sorted position: saturated in the int16 pass
   int* d_list8 = nullptr;         // ascending flagged positions (int8 -> int16)
@@ -238,6 +294,7 @@ struct sw_db {
   GroupDesc* d_mgroups = nullptr; // mini-group layout of the int8-flagged subjects
   uint2* d_mwords = nullptr;
   uint8_t* d_prof8b = nullptr;    // biased uint8 profile of the int8 stage
+  size_t prof8b_cap = 0;
   // f1 batched queries: second query's int8 profile, pair profile, its scores and flags
   int8_t* d_prof_b = nullptr;
   size_t prof_b_cap = 0;
@@ -250,13 +307,18 @@ struct sw_db {
   swk::SelState* d_sel = nullptr;
   long long* d_topk_ids = nullptr;
   int* d_topk_scores = nullptr;
-  int topk_cap = 0;
+  size_t topk_cap = 0;
   void* d_cub = nullptr;
   size_t cub_bytes = 0;
 
-  uint8_t* h_stage = nullptr;     // pinned staging for query + matrix
+  // pinned staging for query + matrix: a ring of slots, each recycled only
+  // after its H2D copy has drained (the async path never waits on a search)
+  static constexpr int kStage = 8;
+  uint8_t* h_stage[kStage] = {};
+  cudaEvent_t ev_stage[kStage] = {};
   size_t stage_cap = 0;
-  cudaEvent_t ev_stage = nullptr, ev_done = nullptr;
+  int stage_next = 0;
+  cudaEvent_t ev_done = nullptr;
   // stage-boundary events of the last kRing searches (sync and async):
   // [0] start, [1] profile done, [2] first pass done, [3] rerun done, [4] ranking done
   static constexpr int kRing = 64;
@@ -266,6 +328,62 @@ struct sw_db {
   int last_n_long = 0;            // groups aligned pair-wise by the intra-task path in the last search
   int last_first_stage = 16;      // lane width of the last search's first pass
 };
+
+// ---- device memory of a handle: the caller's hooks or cudaMalloc ----
+int dalloc(sw_db* db, void** p, size_t bytes) {
+  *p = nullptr;
+  bytes = std::max<size_t>(bytes, 16);
+  if (db->alloc_fn) {
+    *p = db->alloc_fn(bytes, db->alloc_ctx);
+    if (!*p) return fail(SW_ENOMEM, "device allocation hook returned NULL for %zu bytes", bytes);
+  } else {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+      *p = nullptr;
+      return fail(e == cudaErrorMemoryAllocation ? SW_ENOMEM : SW_ECUDA, "cudaMalloc(%zu): %s", bytes,
+                  cudaGetErrorString(e));
+    }
+  }
+  db->n_device_allocs++;
+  db->device_bytes += (int64_t)bytes;
+  db->live.emplace_back(*p, bytes);
+  return SW_OK;
+}
+template <class T>
+int dalloc_t(sw_db* db, T** p, size_t bytes) {
+  void* v = nullptr;
+  const int rc = dalloc(db, &v, bytes);
+  *p = (T*)v;
+  return rc;
+}
+void dfree(sw_db* db, void* p) {
+  if (!p) return;
+  for (size_t t = 0; t < db->live.size(); t++)
+    if (db->live[t].first == p) {
+      db->device_bytes -= (int64_t)db->live[t].second;
+      db->live[t] = db->live.back();
+      db->live.pop_back();
+      break;
+    }
+  if (db->free_fn) db->free_fn(p, db->alloc_ctx);
+  else cudaFree(p);
+}
+// grow-only buffer (blocking paths only: the caller has made the handle idle)
+template <class T>
+int grow(sw_db* db, T** p, size_t* cap, size_t need) {
+  if (*p && *cap >= need) return SW_OK;
+  dfree(db, *p);
+  *p = nullptr;
+  *cap = 0;
+  int rc = dalloc_t(db, p, need);
+  if (rc == SW_OK) *cap = std::max<size_t>(need, 16);
+  return rc;
+}
+#define CK_RC(expr)                 \
+  do {                              \
+    const int _rc = (expr);         \
+    if (_rc != SW_OK) return _rc;   \
+  } while (0)
 
 extern "C" {
 

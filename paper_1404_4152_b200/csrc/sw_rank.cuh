@@ -77,13 +77,19 @@ __global__ void __launch_bounds__(256) k_sel_pick(SelState* st, int shift, unsig
   hist[d] = 0;
 }
 
+// Keys >= the k-th largest: exactly cap = min(k, n) of them, because keys are
+// unique (sw_db_create rejects repeated global ids); the bound check only
+// keeps a violated invariant from writing past `out`.
 __global__ void k_sel_compact(const unsigned long long* __restrict__ keys, int n,
                               const SelState* __restrict__ st, int take_all,
-                              unsigned long long* __restrict__ out, int* __restrict__ count) {
+                              unsigned long long* __restrict__ out, int* __restrict__ count, int cap) {
   const unsigned long long thr = take_all ? 0ull : st->prefix;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     const unsigned long long key = keys[p];
-    if (key >= thr) out[atomicAdd(count, 1)] = key;
+    if (key >= thr) {
+      const int slot = atomicAdd(count, 1);
+      if (slot < cap) out[slot] = key;
+    }
   }
 }
 
@@ -185,7 +191,10 @@ __global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* _
   __syncthreads();
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
     const unsigned long long key = keys[p];
-    if (key >= thr) s[atomicAdd(&sh_cnt, 1)] = key;
+    if (key >= thr) {
+      const int slot = atomicAdd(&sh_cnt, 1);
+      if (slot < cnt) s[slot] = key;   // exactly cnt pass (unique keys); bound kept for safety
+    }
   }
   __syncthreads();
   int n2 = 1;

@@ -41,6 +41,38 @@ int swgen_residues(uint64_t key, uint64_t start, int64_t n, const uint8_t* lut, 
   return 0;
 }
 
+/* Many runs at once (a shard of scattered ids):
+ * out[out_off[r] + i] = lut[draw(key, gstart[r] + i) >> 48], i in [0, len[r]) */
+typedef struct { uint64_t key; const int64_t *gstart, *len, *out_off; int64_t a, b; const uint8_t* lut; uint8_t* out; } runs_t;
+
+static void* runs_worker(void* p) {
+  runs_t* j = (runs_t*)p;
+  for (int64_t r = j->a; r < j->b; r++) {
+    uint8_t* o = j->out + j->out_off[r];
+    const uint64_t g = (uint64_t)j->gstart[r];
+    for (int64_t i = 0; i < j->len[r]; i++) o[i] = j->lut[draw(j->key, g + (uint64_t)i) >> 48];
+  }
+  return NULL;
+}
+
+int swgen_residues_runs(uint64_t key, const int64_t* gstart, const int64_t* len, const int64_t* out_off, int64_t nruns,
+                        const uint8_t* lut, uint8_t* out, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nruns < 4096) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  runs_t jobs[256];
+  for (int t = 0; t < nthreads; t++) {
+    jobs[t].key = key; jobs[t].gstart = gstart; jobs[t].len = len; jobs[t].out_off = out_off;
+    jobs[t].lut = lut; jobs[t].out = out;
+    jobs[t].a = nruns * t / nthreads; jobs[t].b = nruns * (t + 1) / nthreads;
+    if (nthreads == 1) runs_worker(&jobs[t]);
+    else pthread_create(&th[t], NULL, runs_worker, &jobs[t]);
+  }
+  if (nthreads > 1) for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+  return 0;
+}
+
 /* C4 planting model (see synth._mutate).  Writes at most cap residues; returns the
  * mutated length (which may exceed cap, in which case out holds a prefix). */
 int64_t swgen_mutate(const uint8_t* q, int64_t m, uint64_t key, const uint8_t* lut, uint8_t* out, int64_t cap) {

@@ -112,6 +112,8 @@ def _clib():
         lib = ctypes.CDLL(path)
         lib.swgen_residues.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        lib.swgen_residues_runs.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         lib.swgen_mutate.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
         lib.swgen_mutate.restype = ctypes.c_int64
@@ -320,11 +322,20 @@ def make_db(cfg: Config | str, seed: int = 0, ids=None, lengths_kind=None) -> Sy
     k = ids.size
     if k:
         brk = np.nonzero(np.diff(ids) != 1)[0] + 1
-        runs = np.split(np.arange(k), brk)
-        for r in runs:
-            a, b = int(r[0]), int(r[-1]) + 1
-            g0, g1 = int(goff[ids[a]]), int(goff[ids[b - 1] + 1])
-            res[offs[a]:offs[a] + (g1 - g0)] = gen_residues(rkey, g0, g1 - g0)
+        first = np.concatenate([[0], brk]).astype(np.int64)          # first position of each run of ids
+        last = np.concatenate([brk, [k]]).astype(np.int64)           # one past its last position
+        g0 = goff[ids[first]]
+        rl = goff[ids[last - 1] + 1] - g0
+        lib = _clib()
+        if lib is not None and first.size > 64:                       # a scattered shard: one C call
+            g0 = np.ascontiguousarray(g0, dtype=np.int64)
+            rl = np.ascontiguousarray(rl, dtype=np.int64)
+            oo = np.ascontiguousarray(offs[first], dtype=np.int64)
+            lib.swgen_residues_runs(rkey, g0.ctypes.data, rl.ctypes.data, oo.ctypes.data, first.size,
+                                    RESIDUE_LUT.ctypes.data, res.ctypes.data, _nthreads())
+        else:
+            for a, s0, n in zip(first.tolist(), g0.tolist(), rl.tolist()):
+                res[offs[a]:offs[a] + n] = gen_residues(rkey, s0, n)
     special = np.nonzero(kind[ids] >= 2)[0]
     if special.size:
         q = make_query(cfg, seed=seed)

@@ -43,8 +43,8 @@ def _create(res, offs, lens, gids=None, **kw):
     return sw.Database(res, offs, lens, global_ids=gids, **kw)
 
 
-@pytest.mark.parametrize("case", ["bad_code", "overrun", "neg_len", "bad_gid", "bad_stage", "bad_residency",
-                                  "stream_int8", "bad_chunk"])
+@pytest.mark.parametrize("case", ["bad_code", "overrun", "neg_len", "bad_gid", "dup_gid", "bad_stage",
+                                  "bad_residency", "stream_int8", "bad_chunk", "bad_tuning", "neg_cap"])
 def test_db_create_validation(case):
     res = np.array([0, 1, 2, 3, 4, 5], dtype=np.uint8)
     offs = np.array([0, 3], dtype=np.int64)
@@ -59,6 +59,12 @@ def test_db_create_validation(case):
         lens[0] = -1
     elif case == "bad_gid":
         gids = np.array([0, 1 << 33], dtype=np.int64)
+    elif case == "dup_gid":            # ranking keys (score<<32 | ~id) must be unique
+        gids = np.array([7, 7], dtype=np.int64)
+    elif case == "bad_tuning":
+        kw["tuning"] = {"tile_rows": 40}
+    elif case == "neg_cap":
+        kw["max_qlen"] = -3
     elif case == "bad_stage":
         kw["first_stage"] = 12
     elif case == "bad_residency":
@@ -70,6 +76,66 @@ def test_db_create_validation(case):
     with pytest.raises(sw.SwError) as ei:
         _create(res, offs, lens, gids, **kw)
     assert ei.value.code == sw.SW_EINVAL
+
+
+def test_distinct_ids_checked_at_any_position():
+    """The duplicate-id check covers large, sparse ids (bitmap up to the max id)."""
+    n = 5000
+    res = np.zeros(n, dtype=np.uint8)
+    offs = np.arange(n, dtype=np.int64)
+    lens = np.ones(n, dtype=np.int32)
+    gids = np.arange(n, dtype=np.int64) * 800_000 + 17          # up to ~4e9 < 2^32 - 1
+    gids[-1] = gids[1234]
+    with pytest.raises(sw.SwError) as ei:
+        _create(res, offs, lens, gids)
+    assert ei.value.code == sw.SW_EINVAL and "repeats" in str(ei.value)
+
+
+def _raw_create(L, **fields):
+    """sw_db_create through the production library with raw sw_opts fields."""
+    res = np.array([0, 1, 2], dtype=np.uint8)
+    offs = np.array([0], dtype=np.int64)
+    lens = np.array([3], dtype=np.int32)
+    o = sw.sw_opts()
+    L.sw_opts_default(ctypes.byref(o))
+    for k, v in fields.items():
+        if k.startswith("tuning."):
+            setattr(o.tuning, k[7:], v)
+        else:
+            setattr(o, k, v)
+    h = ctypes.c_void_p()
+    rc = L.sw_db_create(res.ctypes.data, 3, offs.ctypes.data, lens.ctypes.data, 1, None, ctypes.byref(o),
+                        ctypes.byref(h))
+    return rc, h
+
+
+@pytest.mark.parametrize("fields", [{"tuning.variant": 1}, {"tuning.tile_rows": 64}, {"tuning.threads": 512},
+                                    {"tuning.intra_cols": 2}, {"tuning.reserved": (ctypes.c_int32 * 2)(1, 0)},
+                                    {"reserved": (ctypes.c_int32 * 4)(0, 1, 0, 0)},
+                                    {"alloc": sw.ALLOC_FN(lambda n, c: None)}])
+def test_production_library_rejects_ablation_switches_and_bad_opts(fields):
+    """Measurement switches are create-time options (never environment variables);
+    the production build accepts only the shipped design; hooks come in pairs."""
+    L = sw.lib()
+    rc, h = _raw_create(L, **fields)
+    assert rc == sw.SW_EINVAL and not h.value, L.sw_last_error()
+    msg = L.sw_last_error().decode()
+    if "tuning.variant" in fields:
+        assert "ablation build" in msg
+
+
+def test_opts_default_capacity():
+    o = sw.sw_opts()
+    sw.lib().sw_opts_default(ctypes.byref(o))
+    assert (o.max_qlen, o.max_k, o.device, o.first_stage) == (8192, 4096, -1, 16)
+    assert not o.alloc and not o.free and o.tuning.variant == 0
+
+
+def test_no_environment_knobs_in_the_library():
+    """No search path reads the environment (getenv per search)."""
+    src = os.path.join(ROOT, "paper_1404_4152_b200", "csrc")
+    for f in os.listdir(src):
+        assert "getenv" not in open(os.path.join(src, f)).read(), f
 
 
 def test_merge_topk_matches_oracle_ranking():

@@ -48,9 +48,9 @@ def _rescore(q, s, M, alpha, beta, a):
     return total
 
 
-def _check(db, q, M, alpha, beta, subjects=None):
+def _check(db, q, M, alpha, beta, subjects=None, **kw):
     subjects = np.arange(db.n_seqs) if subjects is None else np.asarray(subjects)
-    with sw.Database(db.residues, db.offsets, db.lengths, device=0) as g:
+    with sw.Database(db.residues, db.offsets, db.lengths, device=0, **kw) as g:
         res = g.search(q, M, alpha, beta, k=1)
         al = g.align(q, M, alpha, beta, subjects)
     assert len(al) == len(subjects)
@@ -112,14 +112,13 @@ def test_asymmetric_matrix():
     _check(db, _query(90, 5), M, 1, 5)
 
 
-def test_repeats_subset_and_batching(monkeypatch):
+def test_repeats_subset_and_batching():
     rng = np.random.default_rng(13)
     db = random_db(14, np.concatenate([rng.integers(0, 600, 80), [3000, 0]]))
     q = _query(300, 6)
     subjects = np.array([80, 3, 3, 81, 0, 79, 80])
     _check(db, q, B62, 2, 12, subjects)
-    monkeypatch.setenv("SW_ALIGN_WORKSPACE", "65536")     # many small batches
-    _check(db, q, B62, 2, 12, np.arange(db.n_seqs))
+    _check(db, q, B62, 2, 12, np.arange(db.n_seqs), tuning={"align_ws_kb": 64})   # many small batches
 
 
 def test_errors():

@@ -1,6 +1,6 @@
 """Uncontended intra-task wavefront: one pair of 3,303-residue subjects, query lengths 8..512 (rows per
-lane TR = 4..16); first-pass time per subject column and per column-row.  SW_INTRA_NC=2|4 selects the
-columns per wavefront step.  python tools/intra_probe.py"""
+lane TR = 4..16); first-pass time per subject column and per column-row.  `python tools/intra_probe.py [2|4]` selects the
+columns per wavefront step (sw_tuning.intra_cols; 2 needs the ablation build)."""
 import os, sys
 sys.path.insert(0, "/root/repo")
 import numpy as np
@@ -12,7 +12,8 @@ n = 3303
 db = random_db(1, np.array([n, n]))
 for m in (8, 32, 64, 128, 144, 256, 512):
     q = gen_residues(stream_key(0, "q", m), 0, m)
-    with sw.Database.from_synth(db, device=0, long_threshold=1) as g:
+    with sw.Database.from_synth(db, device=0, long_threshold=1,
+                                tuning={"intra_cols": int(sys.argv[1]) if len(sys.argv) > 1 else 0}) as g:
         for _ in range(3):
             g.search(q, M, 2, 12, k=1)
         t = min(g.search(q, M, 2, 12, k=1).stats["ms_inter"] for _ in range(5))

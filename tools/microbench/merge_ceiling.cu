@@ -1,0 +1,134 @@
+// Substitution-merge variants of the int16x2 cell update with the profile in
+// SHARED MEMORY and random residues per column (the k_inter16 tile loop
+// without the packed-word decode and boundary traffic).  One lane holds two
+// subjects (lo/hi halves); per row the pair (fsbt(q_i, s_lo), fsbt(q_i, s_hi))
+// must be formed from two independent table lookups.
+//   MODE 0  int8 table, LDS.64 per 8 rows per subject, PRMT (alu) per row (production)
+//   MODE 1  32-bit tables LO = zext16(s), HI = s << 16; LDS.64 per 2 rows per
+//           subject; D = VIADD2(VIADD2(Hprev, HI), LO): no alu op for the merge
+//   MODE 2  one 32-bit zext table, D = VIADD2(IMAD(T_hi, 0x10000, Hprev), T_lo)
+//   MODE 3+x mixed: rows (r % 8) < NP use MODE 0, the others MODE 1
+// Reports Gcell/s (2 cells per lane-row) at 384 threads / SM.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o merge_ceiling merge_ceiling.cu
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r; asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel)); return r; }
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r; asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r; }
+__device__ __forceinline__ uint2 lds64(const void* p) {
+  uint2 v; asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"((uint32_t)__cvta_generic_to_shared(p))); return v; }
+__host__ __device__ constexpr uint32_t sel_pair(int rr) {
+  return (uint32_t)(rr | ((rr | 8) << 4) | ((4 + rr) << 8) | (((4 + rr) | 8) << 12)); }
+
+constexpr int M = 480;          // query rows held in the tables (tile offset i0 cycles over them)
+
+template <int MODE, int NP, int R = 48, int NT = 384>
+__global__ void __launch_bounds__(NT, 1) k(uint32_t* out, int ncols, int s8, int s32) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  int8_t* p8 = (int8_t*)sm;                                   // [25][s8] bytes
+  uint32_t* lo32 = (uint32_t*)(sm + ((25 * s8 + 15) / 16) * 16);   // [25][s32]
+  uint32_t* hi32 = lo32 + 25 * s32;
+  for (int t = threadIdx.x; t < 25 * s8; t += blockDim.x) {
+    const int r = t / s8, i = t % s8;
+    p8[t] = r == 24 ? 0 : (int8_t)(((r * 7 + i * 13) % 15) - 4);
+  }
+  for (int t = threadIdx.x; t < 25 * s32; t += blockDim.x) {
+    const int r = t / s32, i = t % s32;
+    const int v = r == 24 ? 0 : (((r * 7 + i * 13) % 15) - 4);
+    lo32[t] = (uint32_t)v & 0xffffu;
+    hi32[t] = (uint32_t)v << 16;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint32_t D[R], F[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) { D[r] = 0; F[r] = 0; }
+  uint32_t e = 0, hmax = 0, na2 = 0xfffefffeu, nb2 = 0xfff4fff4u;
+  uint32_t w = 0x9e3779b9u * (threadIdx.x + 1 + blockIdx.x * 977);
+  const int i0 = R * (blockIdx.x % (M / R));
+  for (int j = 0; j < ncols; j++) {
+    w = w * 1664525u + 1013904223u;
+    const uint32_t rlo = ((w >> 24) * 25u) >> 8, rhi = (((w >> 16) & 255u) * 25u) >> 8;
+    const int8_t* a8 = p8 + rlo * s8 + i0;
+    const int8_t* b8 = p8 + rhi * s8 + i0;
+    const uint32_t* a32 = (MODE == 1 || MODE >= 3 ? lo32 : lo32) + rlo * s32 + i0;
+    const uint32_t* b32 = (MODE == 2 ? lo32 : hi32) + rhi * s32 + i0;
+    uint32_t hprev = e ^ (uint32_t)j, hodd = 0;
+    e = 0;
+#pragma unroll
+    for (int k8 = 0; k8 < R / 8; k8++) {
+      uint2 a, b, la, lb;
+      if (MODE == 0 || MODE >= 3) {
+        a = *reinterpret_cast<const uint2*>(a8 + 8 * k8);
+        b = *reinterpret_cast<const uint2*>(b8 + 8 * k8);
+      }
+#pragma unroll
+      for (int rr = 0; rr < 8; rr++) {
+        const int r = 8 * k8 + rr;
+        const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);
+        const bool use_prmt = MODE == 0 || (MODE >= 3 && rr < NP);
+        if (use_prmt) {
+          const uint32_t sn = prmt(rr < 4 ? a.x : a.y, rr < 4 ? b.x : b.y, sel_pair(rr & 3));
+          D[r] = __vadd2(hprev, sn);
+        } else {
+          if (!(r & 1) || (MODE >= 3 && rr == NP)) { la = lds64(a32 + (r & ~1)); lb = lds64(b32 + (r & ~1)); }
+          const uint32_t lv = (r & 1) ? la.y : la.x, hv = (r & 1) ? lb.y : lb.x;
+          if (MODE == 2) D[r] = __vadd2(imad(hv, 0x10000u, hprev), lv);
+          else D[r] = __vadd2(__vadd2(hprev, hv), lv);
+        }
+        const uint32_t hb = __vadd2(h, nb2);
+        e = __viaddmax_s16x2_relu(e, na2, hb);
+        F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+        if (rr & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
+        else hodd = h;
+        hprev = h;
+      }
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = hmax ^ e;
+}
+
+template <int MODE, int NP = 0, int R = 48, int NT = 384>
+void run(const char* name, uint32_t* d_out, int nsm, int s32) {
+  const int ncols = 4096, threads = NT;
+  const int s8 = M + 8;
+  const size_t smem = ((25 * s8 + 15) / 16) * 16 + 2 * 25 * (size_t)s32 * 4;
+  cudaFuncSetAttribute(k<MODE, NP, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; rep++) {
+    cudaEventRecord(e0); k<MODE, NP, R, NT><<<nsm, threads, smem>>>(d_out, ncols, s8, s32); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); float ms; cudaEventElapsedTime(&ms, e0, e1); if (rep && ms < best) best = ms;
+  }
+  cudaError_t err = cudaGetLastError();
+  const double cells = 2.0 * R * ncols * threads * (double)nsm;
+  printf("%-34s R=%d NT=%d s32=%d  %.1f Gcell/s %s\n", name, R, NT, s32, cells / (best * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
+}
+int main() {
+  int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  uint32_t* d_out; cudaMalloc(&d_out, 4 * nsm * 512);
+  if (getenv("TILES")) {
+    run<0, 0, 48, 384>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 32, 512>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 64, 256>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 80, 256>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 96, 256>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 120, 256>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 96, 320>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 64, 320>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 40, 384>("mode0", d_out, nsm, M + 2);
+    return 0;
+  }
+  for (int s32 : {M + 2, M + 4, M + 1 + 1 + 32}) {
+    run<0>("mode0 int8+PRMT", d_out, nsm, s32);
+    run<1>("mode1 32b VIADD2 x2", d_out, nsm, s32);
+    run<2>("mode2 32b IMAD+VIADD2", d_out, nsm, s32);
+    run<3, 6>("mode3 mixed 6/8 PRMT", d_out, nsm, s32);
+    run<3, 4>("mode3 mixed 4/8 PRMT", d_out, nsm, s32);
+    run<3, 2>("mode3 mixed 2/8 PRMT", d_out, nsm, s32);
+    run<3, 1>("mode3 mixed 1/8 PRMT", d_out, nsm, s32);
+  }
+  return 0;
+}

@@ -1,4 +1,4 @@
-"""f4 measurement: first-pass device time of each kernel variant (SW_VARIANT) on C2 (and C4).
+"""f4 measurement: first-pass device time of each kernel variant (sw_tuning.variant, ablation build) on C2 (and C4).
     python tools/run_ablation.py [--configs C2,C4] [--variants base,intersp]"""
 import argparse
 import json
@@ -14,7 +14,7 @@ import numpy as np
 import paper_1404_4152_b200 as sw
 from swdata import CONFIGS, make_db, make_query
 cfg = CONFIGS[sys.argv[1]]; sdb = make_db(cfg); q = make_query(cfg); M = cfg.matrix32()
-g = sw.Database.from_synth(sdb, device=0)
+g = sw.Database.from_synth(sdb, device=0, **json.loads(sys.argv[2]))
 for _ in range(2): g.search(q, M, cfg.alpha, cfg.beta, k=cfg.k)
 rs = [g.search(q, M, cfg.alpha, cfg.beta, k=cfg.k) for _ in range(3)]
 t = min(r.stats["ms_inter"] for r in rs)
@@ -30,14 +30,12 @@ a = ap.parse_args()
 rows = []
 for cfgname in a.configs.split(","):
     for v in a.variants.split(","):
-        env = dict(os.environ)
-        env.pop("SW_VARIANT", None)
-        env.pop("SW_LONG_COLS", None)
+        kw = {}
         if v in ("intersp", "intraqp", "static"):
-            env["SW_VARIANT"] = v
+            kw["tuning"] = {"variant": v}
         if v in ("intra", "intraqp"):                    # every group through the intra-task path
-            env["SW_LONG_COLS"] = "1"
-        out = subprocess.run([sys.executable, "-c", code, cfgname], env=env, capture_output=True, text=True)
+            kw["long_threshold"] = 1
+        out = subprocess.run([sys.executable, "-c", code, cfgname, json.dumps(kw)], capture_output=True, text=True)
         try:
             res = json.loads(out.stdout.strip().splitlines()[-1])
         except Exception:
