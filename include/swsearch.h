@@ -80,7 +80,12 @@ typedef struct sw_tuning {
   int32_t max_big;        /* inter-task groups wider than a warp's boundary slab that get a slab of
                              their own: 0 = up to 2,048; > 0 at most this many; -1 none (tests) */
   int32_t align_ws_kb;    /* sw_align direction workspace per batch in KiB: 0 = 1 GiB (tests force batching) */
-  int32_t reserved[2];    /* must be 0 */
+  int32_t pipeline;       /* 1 = the pipelined first pass k_inter16_pipe: query tiles of a group on
+                             consecutive warps, tile-edge rows through shared-memory rings (DRAM traffic
+                             of the first pass ~50x lower, measured ~11% slower) instead
+                             of per-warp global slabs (k_inter16, default) */
+  int32_t pipe_chain;     /* warps per pipeline chain: 0 = 3 (one SM sub-partition); 1, 6 or 12
+                             (ablation build) */
 } sw_tuning;
 
 typedef struct sw_opts {

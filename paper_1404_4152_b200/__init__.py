@@ -35,7 +35,7 @@ class SwError(RuntimeError):
 class sw_tuning(ctypes.Structure):
     _fields_ = [("variant", ctypes.c_int32), ("tile_rows", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("intra_cols", ctypes.c_int32), ("max_big", ctypes.c_int32), ("align_ws_kb", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("pipeline", ctypes.c_int32), ("pipe_chain", ctypes.c_int32)]
 
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
@@ -197,7 +197,7 @@ def _needs_ablation(tuning) -> bool:
     v = t.get("variant", 0)
     v = VARIANTS[v] if isinstance(v, str) else v
     return bool(v) or t.get("tile_rows", 0) not in (0, 48) or t.get("threads", 0) not in (0, 384) \
-        or t.get("intra_cols", 0) == 2
+        or t.get("intra_cols", 0) == 2 or t.get("pipe_chain", 0) not in (0, 3)
 
 
 def _ptr(a) -> int | None:

@@ -61,12 +61,17 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+// On a CUDA error: report it and clear the runtime's last-error slot, so a
+// non-sticky error (e.g. an invalid launch) is not reported again by the next,
+// unrelated cudaGetLastError() of a later call.
 #define CK(call)                                                                          \
   do {                                                                                    \
     cudaError_t _e = (call);                                                              \
-    if (_e != cudaSuccess)                                                                \
+    if (_e != cudaSuccess) {                                                              \
+      cudaGetLastError();                                                                 \
       return fail(_e == cudaErrorMemoryAllocation ? SW_ENOMEM : SW_ECUDA, "%s: %s (%s:%d)", \
                   #call, cudaGetErrorString(_e), __FILE__, __LINE__);                     \
+    }                                                                                     \
   } while (0)
 
 constexpr int kTileRows = 48;        // query rows per register tile (sw_tuning.tile_rows: 32/64 in the ablation build)
@@ -97,12 +102,18 @@ int raise_smem_limit(const void* fn, size_t bytes) {
     if (e.first.first == dev && e.first.second == fn) {
       if (e.second >= bytes) return SW_OK;
       cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      if (r != cudaSuccess) return fail(SW_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(r));
+      if (r != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SW_ECUDA, "cudaFuncSetAttribute(%zu B): %s", bytes, cudaGetErrorString(r));
+      }
       e.second = bytes;
       return SW_OK;
     }
   cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(bytes, 1));
-  if (r != cudaSuccess) return fail(SW_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(r));
+  if (r != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SW_ECUDA, "cudaFuncSetAttribute(%zu B): %s", bytes, cudaGetErrorString(r));
+  }
   set.push_back({{dev, fn}, bytes});
   return SW_OK;
 }
@@ -141,6 +152,35 @@ inline void* inter16_select(int T, int nt, bool smem, bool big, bool static_sche
   return inter16_kernel<48, 384>(smem, big);
 }
 constexpr int kMaxSmemProfile = 200 * 1024;
+constexpr size_t kSmemOptin = 227 * 1024 - 4096;  // B200 shared memory per block minus the kernels' static smem
+
+// Ring slots per link of the pipelined first pass for a profile of prof_bytes
+// (8, or 4 / 2 for long queries: the more slack between the warps the better), 0 if the profile and the rings do not fit shared
+// memory (the slab kernel k_inter16 then runs).
+// The pipelined first-pass instance: NS ring slots, CL warps per chain.
+template <int CL>
+void* pipe_kernel_ns(int ns) {
+  if (ns == 8) return (void*)swk::k_inter16_pipe<kTileRows, true, swk::kInterThreads, 8, CL>;
+  if (ns == 4) return (void*)swk::k_inter16_pipe<kTileRows, true, swk::kInterThreads, 4, CL>;
+  return (void*)swk::k_inter16_pipe<kTileRows, true, swk::kInterThreads, 2, CL>;
+}
+inline void* pipe_kernel(int ns, int chain) {
+#ifdef SW_ABLATION
+  if (chain == 1) return pipe_kernel_ns<1>(ns);
+  if (chain == 6) return pipe_kernel_ns<6>(ns);
+  if (chain == 12) return pipe_kernel_ns<12>(ns);
+#else
+  (void)chain;
+#endif
+  return pipe_kernel_ns<3>(ns);
+}
+
+inline int pipe_chains(int chain) { return (swk::kInterThreads / 32) / (chain ? chain : 3); }
+inline int pipe_slots_for(size_t prof_bytes, int chain = 0) {
+  for (int ns : {8, 4, 2})
+    if (prof_bytes + swk::pipe_ring_bytes(swk::kInterThreads / 32, ns, pipe_chains(chain)) <= kSmemOptin) return ns;
+  return 0;
+}
 
 // Shape of the intra-task wavefront's blocked profile: TR rows per lane, the
 // fewest that put the query in one 32-lane pass (TR in {4, 6, 8, 12, 16}; longer
@@ -228,7 +268,8 @@ struct sw_db {
   // capacity of the per-search buffers (sw_opts.max_qlen / max_k, sw_db_reserve)
   int cap_qlen = 0, cap_k = 0;
   // inter/intra split and wide-group slabs: a property of the layout, planned at create
-  int split_cut = 0;              // groups with ncols > split_cut go intra-task (pair by pair)
+  int split_cut = 0;              // groups with ncols > split_cut go intra-task (pair by pair), slab kernel
+  int lb_cut = 0;                 // the same split for the pipelined first pass (load balance only)
   int n_big = 0;                  // inter-task groups wider than a warp slab with a slab of their own
   long long big_cols = 0;         // columns per big slab
 
@@ -256,6 +297,8 @@ struct sw_db {
   int* d_inv = nullptr;           // input index -> sorted position (built on the first sw_align)
   uint2* d_big = nullptr;         // boundary slabs of the inter-task groups wider than a warp's slab
   size_t big_cap = 0;
+  uint2* d_pipe_slab = nullptr;   // k_inter16_pipe: per CTA two round-crossing tile-edge slabs
+  long long pipe_slab_cols = 0;
   int8_t* d_profb = nullptr;      // blocked profile of the intra-task wavefront (and f1's second query)
   int8_t* d_profb2 = nullptr;
   size_t profb_cap = 0, profb2_cap = 0;
@@ -409,6 +452,17 @@ int sw_encode(const char* text, int64_t n, uint8_t* out) {
   for (int64_t i = 0; i < n; i++) out[i] = lut[(unsigned char)text[i]];
   return SW_OK;
 }
+
+#ifdef SW_PIPE_PROF
+// Debug build only: read and clear the pipeline's per-warp cycle counters.
+int sw_debug_pipe_counters(unsigned long long* out) {
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out, swk::g_pipe_prof, sizeof(swk::g_pipe_prof)));
+  static const unsigned long long zero[16][8] = {};
+  CK(cudaMemcpyToSymbol(swk::g_pipe_prof, zero, sizeof zero));
+  return SW_OK;
+}
+#endif
 
 // Host merge of per-device top-k lists (the multi-GPU exchange step, DESIGN.md §"Multi-GPU").
 int sw_merge_topk(const int64_t* ids, const int32_t* scores, int32_t n_lists, int32_t k_in, int32_t k_out,

@@ -1,6 +1,7 @@
 // sw_common.cuh -- constants, the group descriptor, PRMT/profile/residue helpers, the query profiles, shared pieces of the persistent kernels
 // Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 

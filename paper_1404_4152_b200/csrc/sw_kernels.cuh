@@ -13,12 +13,16 @@
 // updated with Blackwell DPX instructions (VIADDMNMX/VIMNMX3 .S16x2).  The
 // 16-bit pass flags any subject whose running max could have wrapped
 // (DESIGN.md §"Saturation"); flagged subjects are re-aligned in int32.
+// The production first pass, k_inter16_pipe (sw_pipe.cuh), runs the query
+// tiles of a group on consecutive warps of a CTA and passes tile-edge rows
+// through shared-memory rings instead of global memory.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "sw_common.cuh"
 #include "sw_int16.cuh"
+#include "sw_pipe.cuh"
 #include "sw_int8.cuh"
 #include "sw_int32.cuh"
 #include "sw_multi.cuh"

@@ -55,6 +55,8 @@ def _case(seed):
     residency = int(rng.integers(0, 2)) if stage != 8 else 0
     opts = dict(first_stage=stage, residency=residency, chunk_mb=int(rng.choice([0, 1, 2])),
                 long_threshold=int(rng.choice([0, -1, 64, 300])))
+    if seed % 5 == 2:                    # the pipelined first pass (sw_tuning.pipeline)
+        opts["tuning"] = {"pipeline": 1}
     k = int(rng.integers(1, 40))
     return db, q, M, alpha, beta, k, opts
 
