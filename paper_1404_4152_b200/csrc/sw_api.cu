@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <chrono>
 #include <cstdarg>
@@ -74,6 +75,7 @@ int fail(int code, const char* fmt, ...) {
     }                                                                                     \
   } while (0)
 
+constexpr int kStreamPieces = 16;   // pieces of a streamed search's first chunk
 constexpr int kTileRows = 48;        // query rows per register tile (sw_tuning.tile_rows: 32/64 in the ablation build)
 
 #ifdef SW_ABLATION
@@ -286,6 +288,9 @@ struct sw_db {
   int64_t chunk_words = 0;
   uint2* d_chunk[2] = {nullptr, nullptr};
   int* d_stream_cnt = nullptr;                       // int32 reruns per chunk
+  long long* h_ready_vals = nullptr;                 // pinned: LLONG_MAX, then each first-chunk piece's start word
+  long long* d_ready_from = nullptr;                 // lowest word of the first chunk known to have landed
+  std::vector<int64_t> piece_first;                  // first group of each first-chunk piece (descending)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
 

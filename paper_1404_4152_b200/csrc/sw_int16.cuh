@@ -507,6 +507,24 @@ __device__ __forceinline__ uint32_t intra_multi16(const uint2* __restrict__ pw, 
   return hmax;
 }
 
+// Streamed databases (f2): the first chunk of a search arrives in pieces while
+// the first pass already runs; ready_from holds the lowest word index known to
+// have landed (written by the copy engine after each piece, longest groups
+// first).  A warp waits here until its group's words are in.  nullptr: no wait.
+__device__ __forceinline__ void wait_words_ready(const long long* ready_from, long long base) {
+  if (ready_from) {
+    if ((threadIdx.x & 31) == 0) {
+      for (;;) {
+        long long v;
+        asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(ready_from) : "memory");
+        if (v <= base) break;
+        __nanosleep(200);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <int T, bool SMEM, int NT, bool BIG = false, bool STATIC = false>
 __global__ void __launch_bounds__(NT, 1)
 k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
@@ -514,7 +532,7 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
           int* __restrict__ score_sorted, uint8_t* __restrict__ flag, long long big_off,
-          long long big_cols, int n_big) {
+          long long big_cols, int n_big, const long long* __restrict__ ready_from) {
   extern __shared__ __align__(16) int8_t sprof[];
   __shared__ int s_split;
   if (n_groups_dev) n_groups = *n_groups_dev;   // mini-group layout of a rerun: size known on device only
@@ -543,6 +561,7 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     if (item >= n_items) break;
     const int g = n_items - 1 - item;
     const GroupDesc gd = groups[g];
+    wait_words_ready(ready_from, gd.base);
     // the n_big longest groups (the first items) are wider than a warp's slab:
     // each has a boundary slab of its own, big_off words from `scratch` (one
     // base pointer keeps the slab accesses of the hot loop __restrict__)
@@ -569,7 +588,8 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
           const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
-          int* __restrict__ score_sorted, uint8_t* __restrict__ flag, const int* __restrict__ len_sorted) {
+          int* __restrict__ score_sorted, uint8_t* __restrict__ flag, const int* __restrict__ len_sorted,
+          const long long* __restrict__ ready_from) {
   // The inter-task kernel may start beside this one (programmatic dependent
   // launch): it only reads what was complete before this grid started.
   asm volatile("griddepcontrol.launch_dependents;");
@@ -603,6 +623,7 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     const int p = 31 - item % 32;
     const GroupDesc gd = groups[g];
     if (2 * p >= gd.count) continue;
+    wait_words_ready(ready_from, gd.base);
     const int ncols = len_sorted ? len_sorted[(long long)g * kGroup + min(2 * p + 1, gd.count - 1)] : gd.ncols;
     uint32_t hm;
     if constexpr (NC == 2)

@@ -7,8 +7,10 @@ are embedded below in the NCBI distribution layout (row/column order
 units).  The transcription is pinned by tests/test_matrices.py: symmetry, the
 published value ranges, the SPEC spot values fsbt(A,A)=4 and fsbt(A,P)=-1
 (SPEC.md:129, 222), W-W being the unique maximum, negative expected score under
-the background composition, and the per-row sums below, which were tallied as
-an independent checksum of each row.
+the background composition, and a second, independent transcription of both
+diagonals and of twenty BLOSUM62 pair scores.  A symmetric, in-range slip in
+an off-diagonal entry outside those pairs would pass; parity is unaffected,
+since the oracle and the device read the same table.
 
 `matrix32()` expands a 24x24 matrix into the 32x32 int8 ABI layout
 (row = query residue, column = subject residue; rows/cols 24..31 zero:

@@ -32,6 +32,25 @@ def test_blosum62():
     assert M[22, 22] == -1                                         # X-X negative (reading R13)
 
 
+# A second transcription, typed independently of the tables in swdata/matrices.py.
+B62_DIAG = dict(A=4, R=5, N=6, D=6, C=9, Q=5, E=5, G=6, H=8, I=4, L=4, K=5, M=5, F=6, P=7, S=4, T=5, W=11,
+                Y=7, V=4, B=4, Z=4, X=-1)
+B50_DIAG = dict(A=5, R=7, N=7, D=8, C=13, Q=7, E=6, G=8, H=10, I=5, L=5, K=6, M=7, F=8, P=10, S=5, T=5, W=15,
+                Y=8, V=5, B=5, Z=5, X=-1)
+B62_PAIRS = dict(WC=-2, WY=2, FY=3, IV=3, LI=2, KR=2, ED=2, HY=2, ST=1, NB=3, DB=4, EZ=4, QZ=3, LM=2, IM=1,
+                 VM=1, FW=1, HN=1, RQ=1, AP=-1)
+
+
+def test_second_transcription_diagonals_and_pairs():
+    for M, diag in ((blosum62(), B62_DIAG), (blosum50(), B50_DIAG)):
+        for c, v in diag.items():
+            assert M[ALPHABET.index(c), ALPHABET.index(c)] == v, c
+    M = blosum62()
+    for pair, v in B62_PAIRS.items():
+        i, j = ALPHABET.index(pair[0]), ALPHABET.index(pair[1])
+        assert M[i, j] == v and M[j, i] == v, pair
+
+
 def test_blosum50():
     M = blosum50()
     _check_common(M, -5, 15, 1)

@@ -45,6 +45,16 @@ def stalls(rep):
                 continue
             if f > 0.01:
                 res[k.replace("smsp__average_warp_latency_issue_stalled_", "").replace(".ratio", "")] = f
+    if not res:   # sm_100 reports: warp-state PC sampling shares instead
+        samp = {}
+        for k, v in d.items():
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued"):
+                try:
+                    samp[k.replace("smsp__pcsamp_warps_issue_stalled_", "")] = float(v.replace(",", ""))
+                except ValueError:
+                    pass
+        tot = sum(samp.values()) or 1.0
+        res = {f"{k} (share of samples)": round(v / tot, 4) for k, v in samp.items() if v / tot > 0.002}
     return dict(sorted(res.items(), key=lambda x: -x[1]))
 
 
@@ -64,10 +74,13 @@ def summarize_rep(rep, prefix, cells=None):
 
     def num(s):
         return float(s.split()[0].replace(",", ""))
+    def nbytes(s):
+        for unit, f in (("Tbyte", 1e12), ("Gbyte", 1e9), ("Mbyte", 1e6), ("Kbyte", 1e3)):
+            if unit in s:
+                return num(s) * f
+        return num(s)
     try:
-        rd = num(main["dram__bytes_read.sum"]) * (1e9 if "Gbyte" in main["dram__bytes_read.sum"] else 1e6 if "Mbyte" in main["dram__bytes_read.sum"] else 1)
-        wr = num(main["dram__bytes_write.sum"]) * (1e9 if "Gbyte" in main["dram__bytes_write.sum"] else 1e6 if "Mbyte" in main["dram__bytes_write.sum"] else 1)
-        summ["dram_bytes_per_launch"] = rd + wr
+        summ["dram_bytes_per_launch"] = nbytes(main["dram__bytes_read.sum"]) + nbytes(main["dram__bytes_write.sum"])
     except Exception:
         pass
     if cells:
