@@ -279,6 +279,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend at N > 1; gloo (CPU collectives) lets tests run several ranks "
+                         "on one GPU, whose kernels never wait on one another")
     args = ap.parse_args()
 
     world = env_int("WORLD_SIZE", 1)
@@ -293,9 +296,15 @@ def main():
     import paper_1404_4152_b200 as sw
     from paper_1404_4152_b200.dist import ShardedSearch
 
+    n_dev = torch.cuda.device_count()
+    local = local % max(n_dev, 1) if args.backend == "gloo" else local   # gloo tests: ranks may share a GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    xdev = "cuda" if args.backend == "nccl" else "cpu"   # device of the host-side collectives' tensors
     t_gen = time.perf_counter()
     base, cfg, shard, q, total_res = build_workload(args.config, world, rank, args.n_per_rank)
     t_gen = time.perf_counter() - t_gen
@@ -334,7 +343,7 @@ def main():
     clk = clocks.stop()
     ms_total = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms_total], dtype=torch.float64, device=xdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
         dist.barrier()
@@ -352,9 +361,9 @@ def main():
     if not args.no_parity:
         n_total = cfg.n_seqs
         if world > 1:
-            full = torch.zeros(n_total, dtype=torch.int32, device="cuda")
-            gid = torch.from_numpy(shard.global_ids).cuda()
-            full[gid] = ss.d_scores[:n]
+            full = torch.zeros(n_total, dtype=torch.int32, device=xdev)
+            gid = torch.from_numpy(shard.global_ids).to(xdev)
+            full[gid] = ss.d_scores[:n].to(xdev)
             dist.reduce(full, dst=0, op=dist.ReduceOp.SUM)      # disjoint shards: a sum is a scatter
             full_h = full.cpu().numpy() if rank == 0 else None
             del full
@@ -376,7 +385,7 @@ def main():
             ss.search(q, M, base.alpha, base.beta, scores=h_scores)
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            t = torch.tensor([dt], dtype=torch.float64, device=xdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": round(cells_total / (dt / args.steps) / 1e9, 2), "unit": "GCUPS",
@@ -400,7 +409,7 @@ def main():
                        "cells_per_step": cells_total, "k": k, "first_stage": args.first_stage,
                        "l2": "inputs larger than L2 (packed DB %.0f MB/GPU > 126 MB)" % (info1["packed_bytes"] / 1e6),
                        "parallelism": (f"{world} ranks, residue-balanced snake shards of one database, "
-                                       f"top-k all_gather (NCCL)") if world > 1 else "1 GPU"},
+                                       f"top-k all_gather ({args.backend})") if world > 1 else "1 GPU"},
             "parity": parity,
             "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak_max, 1),
                          "unit": "Gcell/s", "frac": round(achieved / peak_max, 4),

@@ -90,3 +90,26 @@ def test_sharded_search_equals_whole_database_oracle(world, name, n):
         B = rec["block"]
         digs = [hashlib.sha256(got[b:b + B].astype("<i4").tobytes()).hexdigest() for b in range(0, got.size, B)]
         assert digs == rec["block_sha256"] and rec["topk_ids"] == ti.tolist()[:len(rec["topk_ids"])]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_multi_rank_branch_on_one_gpu(world):
+    """bench.py's N > 1 path (never executed): torchrun N ranks on the one GPU with
+    the gloo backend -- each rank generates and searches its snake shard of C1, the top-k goes
+    through all_gather + sw_merge_topk, the device times are reduced with MAX, and rank 0's parity gate
+    checks every subject against the stored C1 oracle digest.  One JSON line, n_gpus = N, strong scaling."""
+    import subprocess
+    import sys
+    root = os.path.dirname(HERE)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", str(world),
+           "--steps", "3", "--warmup", "3", "--config", "C1", "--backend", "gloo", "--no-cpu-baseline"]
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == world and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["seqs_total"] == CONFIGS["C1"].n_seqs and d["config"]["seqs_rank0"] < CONFIGS["C1"].n_seqs
+    assert d["parity"]["ok"] and d["parity"]["blocks_ok"] == d["parity"]["blocks"]
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
