@@ -205,7 +205,7 @@ IntraShape intra_shape(int m_pad) {
 }
 template <int NC>
 void* intra_kernel_nc(const IntraShape& sh) {
-  static_assert(NC == 2 || NC == 4, "columns per step");
+  static_assert(NC == 2 || NC == 4 || NC == 8, "columns per step");
   switch (sh.tr) {
     case 4: return sh.smem ? (void*)swk::k_intra16<4, true, NC> : (void*)swk::k_intra16<4, false, NC>;
     case 5: return sh.smem ? (void*)swk::k_intra16<5, true, NC> : (void*)swk::k_intra16<5, false, NC>;
@@ -223,9 +223,8 @@ void* intra_kernel_nc(const IntraShape& sh) {
 void* intra_kernel(const IntraShape& sh, int intra_cols) {
 #ifdef SW_ABLATION
   if (intra_cols == 2) return intra_kernel_nc<2>(sh);
-#else
-  (void)intra_cols;
 #endif
+  if (intra_cols == 8) return intra_kernel_nc<8>(sh);
   return intra_kernel_nc<4>(sh);
 }
 

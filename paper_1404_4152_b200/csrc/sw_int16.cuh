@@ -405,7 +405,7 @@ __device__ __forceinline__ uint32_t intra_multi16(const uint2* __restrict__ pw, 
                                                   const int8_t* __restrict__ gprof, int stride, int m_pad,
                                                   uint2* __restrict__ gbnd, long long gstride,
                                                   uint32_t na2, uint32_t nb2, int lane) {
-  static_assert(NC == 2 || NC == 4, "columns per step");
+  static_assert(NC == 2 || NC == 4 || NC == 8, "columns per step");
   constexpr int NR = NC / 2;                                              // residue words (4 codes each)
   const int8_t* prof = prof_base<SMEM>(gprof);
   uint32_t hmax = 0u;

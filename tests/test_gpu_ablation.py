@@ -53,10 +53,11 @@ def test_variant_saturation(variant, m):
     assert np.array_equal(r.scores, ref) and r.stats["n_rerun32"] >= 1
 
 
-@pytest.mark.parametrize("nc", [2, 4])
+@pytest.mark.parametrize("nc", [2, 4, 8])
 @pytest.mark.parametrize("m", [1, 8, 129, 144, 300, 600, 1100])
 def test_intra_columns_per_step(nc, m):
-    """The intra-task wavefront with 2 (previous design, ablation build) or 4 (default) columns per step,
+    """The intra-task wavefront with 2 (previous design, ablation build), 4 (throughput) or 8 (latency-bound
+    small databases) columns per step,
     every group forced through it: exact, across rows-per-lane shapes, multi-pass queries, ragged
     column counts (every ncols mod 4) and int32 reruns of planted copies."""
     rng = np.random.default_rng(50 + m)
