@@ -13,7 +13,7 @@
 // then includes the ABI in parts -- sw_db.inc (create / save / load / info),
 // sw_search.inc (sw_search, sw_search_async, streamed databases),
 // sw_batch.inc (f1), sw_align_host.inc (f3) -- and ends with sw_merge_topk.
-// Device code: sw_kernels.cuh (search: sw_common / sw_int16 / sw_int8 / sw_int32
+// Device code (overview in sw_common.cuh; search: sw_common / sw_int16 / sw_pipe / sw_int8 / sw_int32
 // / sw_multi / sw_escalate / sw_rank .cuh), sw_align.cuh (f3), sw_ablation.cuh (f4).
 #include <cuda_runtime.h>
 
@@ -40,7 +40,14 @@
 #include <unistd.h>
 
 #include "../../include/swsearch.h"
-#include "sw_kernels.cuh"
+#include "sw_common.cuh"
+#include "sw_int16.cuh"
+#include "sw_pipe.cuh"
+#include "sw_int8.cuh"
+#include "sw_int32.cuh"
+#include "sw_multi.cuh"
+#include "sw_escalate.cuh"
+#include "sw_rank.cuh"
 #include "sw_align.cuh"
 #ifdef SW_ABLATION
 #include "sw_ablation.cuh"   // f4 kernels: only in the ablation build (libswsearch_ablation.so)

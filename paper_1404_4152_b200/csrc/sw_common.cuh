@@ -1,5 +1,27 @@
 // sw_common.cuh -- constants, the group descriptor, PRMT/profile/residue helpers, the query profiles, shared pieces of the persistent kernels
-// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+//
+// The sm_100a device code of the Smith-Waterman database search (overview).
+//
+// Every kernel computes (part of) Eq. 1 of PAPER.md:31-35 (§II.A):
+//   H(i,j) = max{0, H(i-1,j-1) + fsbt(q_i, s_j), E(i,j), F(i,j)}
+//   E(i,j) = max{E(i-1,j) - alpha, H(i-1,j) - beta}
+//   F(i,j) = max{F(i,j-1) - alpha, H(i,j-1) - beta}
+// with E and F clamped at 0 (exact: DESIGN.md §"Clamped gaps", SURVEY.md
+// Appendix B1), in linear space.  i runs over the query
+// (rows, held in registers per tile), j over the subject (columns, streamed).
+//
+// Inter-task model: one lane aligns one pair of
+// length-sorted subjects, packed as the lo/hi halves of int16x2 registers and
+// updated with Blackwell DPX instructions (VIADDMNMX/VIMNMX3 .S16x2).  The
+// 16-bit pass flags any subject whose running max could have wrapped
+// (DESIGN.md §"Saturation"); flagged subjects are re-aligned in int32.
+// The first pass is k_inter16 (sw_int16.cuh: 48-row register tiles, tile-edge
+// rows in per-warp global slabs); k_inter16_pipe (sw_pipe.cuh, an option) runs
+// the query tiles of a group on consecutive warps of a CTA and passes the
+// tile-edge rows through shared-memory rings instead.
+// Headers: sw_common (this), sw_int16 (first pass, intra-task wavefront),
+// sw_pipe (pipelined first pass), sw_int8, sw_int32 (reruns), sw_multi (f1),
+// sw_escalate (compaction), sw_rank (a6), sw_align (f3), sw_ablation (f4).
 #pragma once
 #include <cstddef>
 #include <cstdint>

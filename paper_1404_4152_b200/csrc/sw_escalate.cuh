@@ -1,5 +1,5 @@
 // sw_escalate.cuh -- a4 escalation plumbing: flag compaction and mini-group re-interleaving
-// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+// Part of the device code of libswsearch (see sw_common.cuh for the overview).
 #pragma once
 #include "sw_common.cuh"
 

@@ -1,5 +1,5 @@
 // sw_int16.cuh -- the int16x2 DPX first pass: cell update, register tiles, inter-task and intra-task kernels (a3, a5)
-// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+// Part of the device code of libswsearch (see sw_common.cuh for the overview).
 #pragma once
 #include "sw_common.cuh"
 

@@ -1,5 +1,5 @@
 // sw_int32.cuh -- the exact int32 pass: reruns of saturated subjects and first_stage 32 (a4)
-// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+// Part of the device code of libswsearch (see sw_common.cuh for the overview).
 #pragma once
 #include "sw_common.cuh"
 

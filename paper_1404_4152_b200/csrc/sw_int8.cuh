@@ -1,5 +1,5 @@
 // sw_int8.cuh -- the optional int8 first stage (a4, biased unsigned bytes)
-// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+// Part of the device code of libswsearch (see sw_common.cuh for the overview).
 #pragma once
 #include "sw_common.cuh"
 

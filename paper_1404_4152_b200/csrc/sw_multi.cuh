@@ -1,5 +1,5 @@
 // sw_multi.cuh -- f1: two queries per int16x2 pass
-// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+// Part of the device code of libswsearch (see sw_common.cuh for the overview).
 #pragma once
 #include "sw_common.cuh"
 

@@ -1,5 +1,5 @@
 // sw_pipe.cuh -- the int16x2 first pass with query tiles pipelined over the warps of a CTA (a3)
-// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+// Part of the device code of libswsearch (see sw_common.cuh for the overview).
 //
 // k_inter16 keeps a 48-row query tile in registers and sweeps it over a
 // 64-subject group; the (E, H) row at every tile edge goes to a per-warp slab in

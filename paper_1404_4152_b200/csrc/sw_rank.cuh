@@ -1,5 +1,5 @@
 // sw_rank.cuh -- a6: scatter to input order and exact top-k
-// Part of the device code of libswsearch (see sw_kernels.cuh for the overview).
+// Part of the device code of libswsearch (see sw_common.cuh for the overview).
 #pragma once
 #include "sw_common.cuh"
 
