@@ -267,6 +267,49 @@ def load_ncu_traffic(config: str = "C5"):
         return {"traffic": None}
 
 
+def c3_sweep(sw, args):
+    """The paper's protocol (§IV.A, Fig. 5): query lengths 144 ... 5,478 against one large
+    database -- here C3 (20M synthetic sequences, 7.39 B residues, 0.1 % 5k-35k tail).  Per query: one warm-up
+    search, one timed search (device CUDA events around the whole search, first-pass time from the library's
+    stage events), and every subject's score against the stored oracle digest."""
+    import torch
+    from swdata import CONFIGS, make_db, make_query
+    cfg = CONFIGS["C3"]
+    t0 = time.perf_counter()
+    sdb = make_db(cfg)
+    n, residues = sdb.n_seqs, int(sdb.lengths.astype(np.int64).sum())
+    db = sw.Database.from_synth(sdb, device=torch.cuda.current_device())
+    setup_s = time.perf_counter() - t0
+    del sdb
+    M = cfg.matrix32()
+    stream = torch.cuda.Stream()
+    d_sc = torch.empty(n, dtype=torch.int32, device="cuda")
+    d_ti = torch.empty(cfg.k, dtype=torch.int64, device="cuda")
+    d_ts = torch.empty(cfg.k, dtype=torch.int32, device="cuda")
+    peak = SMS * 1965e6 * ALU_LANES_PER_CLK / ALU_OPS_PER_CELL / 1e9
+    rows = []
+    for m in cfg.qlens:
+        q = make_query(cfg, m)
+        db.search_async(q, M, cfg.alpha, cfg.beta, cfg.k, d_sc, d_ti, d_ts, stream=stream)   # warm-up
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        db.search_async(q, M, cfg.alpha, cfg.beta, cfg.k, d_sc, d_ti, d_ts, stream=stream)
+        e1.record(stream)
+        stream.synchronize()
+        ms = e0.elapsed_time(e1)
+        ms_first = db.stage_times(1)[1]
+        cells = m * residues
+        par = parity_gate(d_sc.cpu().numpy(), d_ti.cpu().numpy(), d_ts.cpu().numpy(), "C3", m, n)
+        rows.append({"m": m, "gcups": round(cells / ms / 1e6, 1), "first_pass_gcups": round(cells / ms_first / 1e6, 1),
+                     "roofline_frac": round(cells / ms_first / 1e6 / peak, 4), "ms": round(ms, 2),
+                     "parity_ok": bool(par.get("ok")), "blocks_ok": par.get("blocks_ok")})
+    db.close()
+    return {"workload": f"C3 (BASELINE.json configs[2]): {n:,} seqs, {residues:,} residues, BLOSUM62 alpha=2 "
+                        f"beta=12, top-{cfg.k}; one timed search per query after one warm-up",
+            "setup_s": round(setup_s, 1), "queries": rows,
+            "gcups_mean": round(sum(r["gcups"] for r in rows) / len(rows), 1)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -280,6 +323,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the C3 query-length sweep (the paper's protocol, PAPER.md:162-166) after the C5 line")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend at N > 1; gloo (CPU collectives) lets tests run several ranks "
                          "on one GPU, whose kernels never wait on one another")
@@ -453,8 +498,12 @@ def main():
             line["cpu_baseline"] = cpu_baseline(base, q, shard)
         elif not args.no_cpu_baseline:
             line["cpu_baseline"] = None
-        print(json.dumps(line), flush=True)
     ss.close()
+    if rank == 0:
+        if world == 1 and not args.no_sweep and args.config == "C5" and not args.n_per_rank:
+            del shard
+            line["c3_sweep"] = c3_sweep(sw, args)
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
