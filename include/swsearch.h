@@ -86,6 +86,10 @@ typedef struct sw_tuning {
                              of per-warp global slabs (k_inter16, default) */
   int32_t pipe_chain;     /* warps per pipeline chain: 0 = 3 (one SM sub-partition); 1, 6 or 12
                              (ablation build) */
+  int32_t intra_isolate;  /* intra-task kernel: 1 = the warps holding the longest pairs get their SM
+                             sub-partition alone, -1 = never, 0 = when the longest pair is the critical
+                             path (small databases such as C1) */
+  int32_t reserved[3];    /* must be 0 */
 } sw_tuning;
 
 typedef struct sw_opts {

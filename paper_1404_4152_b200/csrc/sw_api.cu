@@ -473,6 +473,20 @@ int sw_debug_pipe_counters(unsigned long long* out) {
   CK(cudaMemcpyToSymbol(swk::g_pipe_prof, zero, sizeof zero));
   return SW_OK;
 }
+int sw_debug_intra_counters(unsigned long long* out) {
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out, swk::g_intra_prof, sizeof(swk::g_intra_prof)));
+  CK(cudaMemcpyFromSymbol(out + 8, swk::g_intra_first, sizeof(swk::g_intra_first)));
+  CK(cudaMemset(nullptr, 0, 0));
+  {
+    void* p = nullptr;
+    CK(cudaGetSymbolAddress(&p, swk::g_intra_first));
+    CK(cudaMemset(p, 0, sizeof(swk::g_intra_first)));
+  }
+  unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+  CK(cudaMemcpyToSymbol(swk::g_intra_prof, init, sizeof init));
+  return SW_OK;
+}
 #endif
 
 // Host merge of per-device top-k lists (the multi-GPU exchange step, DESIGN.md §"Multi-GPU").

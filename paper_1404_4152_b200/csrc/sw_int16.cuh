@@ -582,6 +582,18 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
 // len_sorted (first pass only; NULL for rerun layouts): each pair runs to its own
 // longer subject's length instead of the group's ncols (the columns past it are
 // DUMMY padding, score-neutral).
+#ifdef SW_PIPE_PROF
+// Debug build only: globaltimer ns of [0] first CTA start (min), [1] last warp end (max),
+// [2]/[3] start/end of item 0 (the longest pair), [4] items taken by that warp afterwards.
+__device__ unsigned long long g_intra_prof[8];
+__device__ unsigned long long g_intra_first[2048][4];   // per warp: first item start, end, ncols, items
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int TR, bool SMEM, int NC = 2>
 __global__ void __launch_bounds__(kInterThreads, 1)
 k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
@@ -589,7 +601,7 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
           int* __restrict__ score_sorted, uint8_t* __restrict__ flag, const int* __restrict__ len_sorted,
-          const long long* __restrict__ ready_from) {
+          const long long* __restrict__ ready_from, int isolate) {
   // The inter-task kernel may start beside this one (programmatic dependent
   // launch): it only reads what was complete before this grid started.
   asm volatile("griddepcontrol.launch_dependents;");
@@ -604,6 +616,9 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
+#ifdef SW_PIPE_PROF
+  if (threadIdx.x == 0) atomicMin(&g_intra_prof[0], gtimer());
+#endif
   if (SMEM) load_profile_smem(sprof, gprof, stride);
   const int lane = threadIdx.x & 31;
   uint2* bnd = scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
@@ -611,8 +626,18 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   // First items are dealt across the SMs (warp k of CTA b takes item k*gridDim.x + b),
   // so the longest pairs -- the wavefront's critical paths -- do not share an SM;
   // the rest come longest-first from the counter.
-  const int n_warps = gridDim.x * (blockDim.x >> 5);
-  int item = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  // Latency-bound searches (isolate = 1: the longest pair's wavefront is the
+  // critical path of the whole pass, e.g. C1): warp 0 of every CTA, which holds
+  // one of the gridDim.x longest pairs, gets its SM sub-partition to itself --
+  // warps 4 and 8 (same sub-partition) take no items and the other warps are
+  // dealt the first items densely.  Measured on C1: the longest pair 316 -> 229 us
+  // (209 us alone on the GPU).
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool idle = isolate && w != 0 && (w & 3) == 0;
+  const int w_active = isolate ? w - (w > 4) - (w > 8) : w;                  // dense index of this warp
+  const int nw_active = isolate ? nw - (nw > 4) - (nw > 8) : nw;
+  const int n_warps = gridDim.x * nw_active;
+  int item = idle ? n_items : w_active * gridDim.x + blockIdx.x;
   for (;; item = -1) {
     if (item < 0) {
       if (lane == 0) item = n_warps + atomicAdd(counter, 1);
@@ -625,17 +650,33 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     if (2 * p >= gd.count) continue;
     wait_words_ready(ready_from, gd.base);
     const int ncols = len_sorted ? len_sorted[(long long)g * kGroup + min(2 * p + 1, gd.count - 1)] : gd.ncols;
+#ifdef SW_PIPE_PROF
+    const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (lane == 0) {
+      if (g_intra_first[wid][3] == 0) { g_intra_first[wid][0] = gtimer(); g_intra_first[wid][2] = ncols; }
+      g_intra_first[wid][3]++;
+    }
+#endif
     uint32_t hm;
     if constexpr (NC == 2)
       hm = intra_pair16<TR, SMEM>(words + gd.base + p, ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
                                   na2, nb2, lane);
+    else if (NC == 4 && isolate && w == 0)   // the isolated warp: 8 columns per step (lower latency per column)
+      hm = intra_multi16<TR, SMEM, 8>(words + gd.base + p, ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
+                                      na2, nb2, lane);
     else
       hm = intra_multi16<TR, SMEM, NC>(words + gd.base + p, ncols, gprof, stride, m_pad, bnd, scratch_cols * 16,
                                        na2, nb2, lane);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) hm = __vmaxs2(hm, __shfl_xor_sync(0xffffffffu, hm, o));
     if (lane == 0) emit_pair(hm, g, 2 * p, gd.count, limit, pos_map, score_sorted, flag);
+#ifdef SW_PIPE_PROF
+    if (lane == 0 && g_intra_first[wid][3] == 1) g_intra_first[wid][1] = gtimer();
+#endif
   }
+#ifdef SW_PIPE_PROF
+  if (lane == 0) atomicMax(&g_intra_prof[1], gtimer());
+#endif
   // When launched as a programmatic dependent (a chain of intra-task passes in
   // sw_search_batch), retire only after the primary grid: a no-op otherwise.
   asm volatile("griddepcontrol.wait;" ::: "memory");
