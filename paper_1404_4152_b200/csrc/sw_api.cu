@@ -422,16 +422,19 @@ void dfree(sw_db* db, void* p) {
   if (db->free_fn) db->free_fn(p, db->alloc_ctx);
   else cudaFree(p);
 }
-// grow-only buffer (blocking paths only: the caller has made the handle idle)
+// grow-only buffer (blocking paths only: the caller has made the handle idle).
+// The new buffer is allocated before the old one is released, so a failed grow
+// (SW_ENOMEM) leaves the handle as it was.
 template <class T>
 int grow(sw_db* db, T** p, size_t* cap, size_t need) {
   if (*p && *cap >= need) return SW_OK;
+  T* fresh = nullptr;
+  const int rc = dalloc_t(db, &fresh, need);
+  if (rc != SW_OK) return rc;
   dfree(db, *p);
-  *p = nullptr;
-  *cap = 0;
-  int rc = dalloc_t(db, p, need);
-  if (rc == SW_OK) *cap = std::max<size_t>(need, 16);
-  return rc;
+  *p = fresh;
+  *cap = std::max<size_t>(need, 16);
+  return SW_OK;
 }
 #define CK_RC(expr)                 \
   do {                              \

@@ -132,3 +132,49 @@ def test_two_handles_from_two_threads_with_different_query_lengths():
     for x in th:
         x.join()
     assert not errors, errors
+
+
+class _FailingAllocator(sw.TorchAllocator):
+    """torch-backed hooks that refuse the (fail_at+1)-th allocation (fault injection)."""
+
+    def __init__(self, device, fail_at):
+        import torch
+        super().__init__(device)
+        self.fail_at = fail_at
+        inner = self.alloc_fn
+
+        def _alloc(nbytes, ctx):
+            if self.n_alloc >= self.fail_at:
+                return None
+            return inner(nbytes, ctx)
+
+        self.alloc_fn = sw.ALLOC_FN(_alloc)
+        self._keep = inner
+
+
+@pytest.mark.parametrize("residency", [0, 1])
+def test_allocation_failure_at_every_step_of_create_is_clean(residency):
+    """Every device allocation of sw_db_create / sw_db_reserve in turn refused: SW_ENOMEM, no handle, and
+    every buffer that was handed out is given back (no leak); one more allocation and create succeeds."""
+    db = _db(31, 300)
+    total = None
+    ok = sw.TorchAllocator(0)
+    with sw.Database.from_synth(db, device=0, allocator=ok, residency=residency) as g:
+        total = g.info()["n_device_allocs"]
+    assert total and ok.n_free == ok.n_alloc == total
+    for fail_at in range(total):
+        a = _FailingAllocator(0, fail_at)
+        with pytest.raises(sw.SwError) as e:
+            sw.Database.from_synth(db, device=0, allocator=a, residency=residency)
+        assert e.value.code == sw.SW_ENOMEM, (fail_at, str(e.value))
+        assert a.n_alloc == fail_at and a.n_free == a.n_alloc and not a.live, fail_at
+    a = _FailingAllocator(0, total)
+    with sw.Database.from_synth(db, device=0, allocator=a, residency=residency) as g:
+        q = _query(120, 5)
+        assert np.array_equal(g.search(q, B62, 2, 12, k=3).scores, oracle.db_scores(q, db, B62, 2, 12))
+        with pytest.raises(sw.SwError) as e:            # growing past the hooks' budget fails cleanly too
+            g.reserve(20000, 5000)
+        assert e.value.code == sw.SW_ENOMEM
+        r = g.search(q, B62, 2, 12, k=3)                 # the handle still works within its old capacity
+        assert np.array_equal(r.scores, oracle.db_scores(q, db, B62, 2, 12))
+    assert a.n_free == a.n_alloc and not a.live

@@ -3,7 +3,8 @@
 Each case checks its scores against the oracle too, so a sanitizer-clean run is also a correct one.
 Sizes are small (the sanitizers slow kernels down 10-100x) but still cover every kernel: int8/16/32
 first stages, saturation reruns, long subjects (intra-task wavefront and big boundary slabs),
-streamed chunks, paired batch queries and the traceback."""
+streamed chunks (first chunk in pieces), paired batch queries, the traceback and the pipelined first
+pass (shared-memory rings with mbarriers)."""
 import argparse
 import os
 import sys
@@ -27,7 +28,7 @@ lens = np.concatenate([rng.integers(0, 400, size=700), [1, 2, 6, 7, 64, 65, 2500
 db = random_db(7, lens)
 q = gen_residues(stream_key(7, "sanitize-query", 200), 0, 200)
 ref = oracle.db_scores(q, db, M, 2, 12)
-cases = a.case.split(",") if a.case != "all" else ["search", "stream", "batch", "align"]
+cases = a.case.split(",") if a.case != "all" else ["search", "stream", "batch", "align", "pipeline"]
 
 
 def check(name, scores, want=ref):
@@ -65,4 +66,9 @@ if "align" in cases:
         al = g.align(q, M, 2, 12, hits)
     got = np.array([x["score"] for x in al])
     check("align scores", got, ref[hits])
+if "pipeline" in cases:   # the pipelined first pass: rings, mbarriers, slabs, cp.async staging
+    for chain in (0, 12):
+        with sw.Database(db.residues, db.offsets, db.lengths, device=0,
+                         tuning={"pipeline": 1, "pipe_chain": chain}) as g:
+            check(f"search pipeline chain={chain or 3}", g.search(q, M, 2, 12, k=10).scores)
 print("sanitize cases done", flush=True)
