@@ -375,8 +375,11 @@ template <int R, int NC>
 __device__ __forceinline__ void col16b_xn(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t (&e)[NC],
                                           uint32_t (&hp)[NC], const uint4 (&pa)[NC], const uint4 (&pb)[NC],
                                           uint32_t na2, uint32_t nb2, uint32_t& hmax) {
-  uint32_t pend = 0u;
-  int npend = 0;
+  // The running max is folded into two accumulators, alternating per pair of
+  // cells, so its dependency chain is half as long as the step's cell count
+  // (one chain serialised the latency-bound wavefront).
+  uint32_t pend = 0u, hmax2 = 0u;
+  int npend = 0, acc = 0;
 #pragma unroll
   for (int r = 0; r < R + NC - 1; r++) {
 #pragma unroll
@@ -391,13 +394,18 @@ __device__ __forceinline__ void col16b_xn(uint32_t (&D)[R], uint32_t (&F)[R], ui
         e[c] = __viaddmax_s16x2_relu(e[c], na2, hb);
         F[q] = __viaddmax_s16x2_relu(F[q], na2, hb);
         hp[c] = h;
-        if (npend) hmax = __vimax3_s16x2(hmax, pend, h);
-        else pend = h;
+        if (npend) {
+          if (acc) hmax2 = __vimax3_s16x2(hmax2, pend, h);
+          else hmax = __vimax3_s16x2(hmax, pend, h);
+          acc ^= 1;
+        } else {
+          pend = h;
+        }
         npend ^= 1;
       }
     }
   }
-  if (npend) hmax = __vmaxs2(hmax, pend);
+  hmax = npend ? __vimax3_s16x2(hmax, hmax2, pend) : __vmaxs2(hmax, hmax2);
 }
 
 template <int TR, bool SMEM, int NC>
