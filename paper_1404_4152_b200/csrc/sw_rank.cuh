@@ -131,8 +131,22 @@ __global__ void __launch_bounds__(1024) k_topk_small(const unsigned long long* _
 // CTA -- radix select of the k-th largest unique key (8 bits per pass, smem
 // histogram), compaction of the k keys above it, bitonic sort, decode --
 // instead of the 19-launch multi-CTA path.
-__global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* __restrict__ keys, int n, int k,
+// The keys are read eight times (one radix pass per byte); when they fit
+// (n <= kTopkSmemKeys) they are staged in dynamic shared memory once, so the
+// passes run at shared-memory latency instead of a chain of dependent global
+// loads per thread (C1: 22 us per ranking before).
+constexpr int kTopkSmemKeys = 12288;              // 96 KB of dynamic shared memory
+
+__global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* __restrict__ gkeys, int n, int k,
                                                      long long* __restrict__ out_ids, int* __restrict__ out_scores) {
+  extern __shared__ unsigned long long skeys[];
+  const bool staged = n <= kTopkSmemKeys;
+  if (staged) {
+#pragma unroll 4
+    for (int p = threadIdx.x; p < n; p += blockDim.x) skeys[p] = gkeys[p];
+    __syncthreads();
+  }
+  const unsigned long long* keys = staged ? skeys : gkeys;
   __shared__ unsigned long long s[4096];
   __shared__ unsigned hist[256];
   __shared__ unsigned long long sh_prefix, sh_mask;
@@ -146,6 +160,7 @@ __global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* _
       for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0u;
       __syncthreads();
       const unsigned long long prefix = sh_prefix, mask = sh_mask;
+#pragma unroll 4
       for (int p = threadIdx.x; p < n; p += blockDim.x) {
         const unsigned long long key = keys[p];
         if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
