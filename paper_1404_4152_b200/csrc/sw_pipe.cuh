@@ -341,7 +341,7 @@ __device__ __forceinline__ void item16p(int out_mode, bool rem_tile, int rem, co
 // runs its own item sequence (rounds of CL items), fetch ticket and
 // round-crossing slab.  Dynamic smem: the profile (SMEM), then the ring (W
 // links x NS slots: link w = warp w -> warp w + NCH), then its mbarriers
-// [full | empty].  slab: per CTA NCH x 2 x slab_cols x 32 uint2.  Groups
+// [full | empty].  slab: per CTA NCH x 2 x slab_cols x 32 uint2 (NCH chains).  Groups
 // [0, split) in the longest-first queue `counter`, as k_inter16 (first-pass
 // layout only).
 template <int T, bool SMEM, int NT, int NS, int CL>
@@ -387,7 +387,7 @@ k_inter16_pipe(const uint2* __restrict__ words, const GroupDesc* __restrict__ gr
   using End = PipeEnd<W, NS>;
   End in{smem_u32(ring), (uint32_t)(pos > 0 ? w - NCH : 0), 0u};   // ring link (pos-1) -> pos
   End out{smem_u32(ring), (uint32_t)w, 0u};                         // ring link pos -> pos+1
-  uint2* const chain_slab = slab + ((long long)blockIdx.x * kMaxChains + c) * 2 * slab_cols * 32 + lane;
+  uint2* const chain_slab = slab + ((long long)blockIdx.x * NCH + c) * 2 * slab_cols * 32 + lane;
   // staging ring of this chain's head (after the ring's mbarriers): kStageCols x 32 uint2
   const uint32_t stage = smem_u32(bars + 2 * W * NS) + (uint32_t)(c * kStageCols * 256 + lane * 8);
 #ifdef SW_PIPE_PROF
