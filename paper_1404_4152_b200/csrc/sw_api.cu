@@ -204,7 +204,11 @@ IntraShape intra_shape(int m_pad) {
   const int need = (m_pad + 31) / 32;
   IntraShape sh;
   sh.tr = need <= 4 ? 4 : need <= 8 ? need : need <= 10 ? 10 : need <= 12 ? 12 : need <= 14 ? 14 : 16;
-  sh.nblk = (m_pad + sh.tr - 1) / sh.tr;
+  // Row stride padded to 128 B: lane l reads block l of the row of ITS column's
+  // residue, so with a 128-B multiple each quarter-warp of an LDS.128 hits 8
+  // distinct 16-B bank groups whatever the residues (m = 144: 464 -> 512 B,
+  // 37.8k bank conflicts per 3,303-column pair before, ncu r02_ncu_intra_pair).
+  sh.nblk = ((m_pad + sh.tr - 1) / sh.tr + 7) & ~7;
   sh.rowstride = sh.nblk * 16;
   sh.bytes = (size_t)swk::kProfRows * sh.rowstride;
   sh.smem = sh.bytes <= (size_t)kMaxSmemProfile;
