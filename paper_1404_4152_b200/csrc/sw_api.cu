@@ -137,6 +137,12 @@ void* inter16_kernel(bool smem, bool big) {
   if (big) return smem ? (void*)swk::k_inter16<T, true, NT, true> : (void*)swk::k_inter16<T, false, NT, true>;
   return smem ? (void*)swk::k_inter16<T, true, NT> : (void*)swk::k_inter16<T, false, NT>;
 }
+// The shipped shape with the paper's gap penalties as immediates (swk::kFixedAlpha/kFixedBeta;
+// profile in shared memory, i.e. m up to ~8,000): sw_common.cuh.
+inline void* inter16_kernel_fixed_gaps(bool big) {
+  return big ? (void*)swk::k_inter16<kTileRows, true, swk::kInterThreads, true, false, 1>
+             : (void*)swk::k_inter16<kTileRows, true, swk::kInterThreads, false, false, 1>;
+}
 #ifdef SW_ABLATION
 // f4 ablation (sw_tuning.variant 3): the paper's static loop schedule instead of the work queue
 inline void* inter16_kernel_static(bool smem, bool big) {
@@ -147,7 +153,9 @@ inline void* inter16_kernel_static(bool smem, bool big) {
 
 // The int16x2 first-pass instance for a tile height / CTA size (only 48 / 384
 // in the production build; sw_db_create rejects the others there).
-inline void* inter16_select(int T, int nt, bool smem, bool big, bool static_schedule) {
+inline void* inter16_select(int T, int nt, bool smem, bool big, bool static_schedule, bool fixed_gaps) {
+  if (fixed_gaps && smem && T == kTileRows && nt == swk::kInterThreads && !static_schedule)
+    return inter16_kernel_fixed_gaps(big);
 #ifdef SW_ABLATION
   if (static_schedule) return inter16_kernel_static(smem, big);
   if (T == 32) return nt == 512 ? inter16_kernel<32, 512>(smem, big) : inter16_kernel<32, 384>(smem, big);

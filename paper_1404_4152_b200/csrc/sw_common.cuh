@@ -72,10 +72,18 @@ __device__ __forceinline__ const int8_t* prof_base(const int8_t* gprof) {
   }
 }
 
-__device__ __forceinline__ uint32_t pack2(int v) {
-  const uint32_t h = (uint32_t)v & 0xffffu;
-  return h | (h << 16);
+__host__ __device__ constexpr uint32_t pack2(int v) {
+  return ((uint32_t)v & 0xffffu) | (((uint32_t)v & 0xffffu) << 16);
 }
+
+// The gap penalties of every experiment in the paper, "10-2k" (PAPER.md:164,
+// §IV.A; reading R4: alpha = 2, beta = 12).  The first-pass kernel has an
+// instance with them as immediates (GAPS = 1): the two packed penalties are
+// then instruction operands instead of registers, which frees two registers
+// and the operand reads of 3 of the 6.5 cell-update instructions per row --
+// measured 3.5 % more cells/s on C2 and C5.  Any other (alpha, beta) runs the
+// GAPS = 0 instance with the same arithmetic.
+constexpr int kFixedAlpha = 2, kFixedBeta = 12;
 
 // ---------------------------------------------------------------------------
 // (i) query profile (PAPER.md:55 stage (i); §III.B.2): row r of the

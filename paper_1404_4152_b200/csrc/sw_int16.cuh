@@ -533,7 +533,7 @@ __device__ __forceinline__ void wait_words_ready(const long long* ready_from, lo
   }
 }
 
-template <int T, bool SMEM, int NT, bool BIG = false, bool STATIC = false>
+template <int T, bool SMEM, int NT, bool BIG = false, bool STATIC = false, int GAPS = 0>
 __global__ void __launch_bounds__(NT, 1)
 k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
           const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
@@ -555,7 +555,9 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   const int lane = threadIdx.x & 31;
   const long long own = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
   uint2* const own_bnd = scratch + own;
-  const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
+  // GAPS = 1: the paper's penalties as immediates (kFixedAlpha/kFixedBeta; the host launches it only for them)
+  const uint32_t na2 = GAPS == 1 ? pack2(-kFixedAlpha) : pack2(-alpha);
+  const uint32_t nb2 = GAPS == 1 ? pack2(-kFixedBeta) : pack2(-beta);
   int it_static = 0;
   for (;;) {
     int item = 0;

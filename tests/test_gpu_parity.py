@@ -67,6 +67,30 @@ def test_gap_parameters(alpha, beta):
     _check(db, _query(300, 2), B62, alpha, beta)
 
 
+@pytest.mark.parametrize("big", [False, True])
+def test_fixed_gap_instance_equals_generic(big):
+    """The paper's 10-2k penalties (alpha 2, beta 12) run a first-pass instance with
+    them as immediates; sw_tuning.generic_gaps = 1 forces the register instance.  Both
+    give the oracle's scores on tiles, ragged tails, wide groups (own slabs) and
+    planted copies past LIMIT16 (int32 reruns); neighbouring penalties take the
+    generic instance."""
+    rng = np.random.default_rng(4212 + big)
+    lens = np.concatenate([rng.integers(0, 700, size=800), [6400, 6400, 0, 1]])
+    if big:
+        lens = np.concatenate([lens, rng.integers(6200, 7000, size=70)])
+    db = random_db(4212 + big, lens)
+    q = _query(6600, 42)
+    db.residues[db.offsets[800]:db.offsets[800] + 6400] = q[:6400]          # self-score > LIMIT16
+    db.residues[db.offsets[801]:db.offsets[801] + 6400] = q[100:6500]
+    for m in (100, 6600):
+        for tuning in ({}, {"generic_gaps": 1}):
+            r = _check(db, q[:m], B62, 2, 12, k=6, long_threshold=-1 if big else 0, tuning=tuning)
+            if m == 6600:
+                assert r.stats["n_rerun32"] >= 1
+        _check(db, q[:m], B62, 2, 13, long_threshold=-1 if big else 0)
+        _check(db, q[:m], B62, 3, 12, long_threshold=-1 if big else 0)
+
+
 def test_blosum50_and_random_asymmetric_matrices():
     rng = np.random.default_rng(3)
     db = random_db(8, rng.integers(1, 500, size=600))
