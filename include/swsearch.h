@@ -89,9 +89,10 @@ typedef struct sw_tuning {
   int32_t intra_isolate;  /* intra-task kernel: 1 = the warps holding the longest pairs get their SM
                              sub-partition alone, -1 = never, 0 = when the longest pair is the critical
                              path (small databases such as C1) */
-  int32_t generic_gaps;   /* 1 = the first pass keeps alpha, beta in registers even for the paper's
-                             10-2k penalties (alpha 2, beta 12), which otherwise run an instance with
-                             them as immediates (~3.5 % faster; identical results) */
+  int32_t generic_gaps;   /* 1 = the int16x2 first-pass kernels (inter-task, intra-task wavefront,
+                             paired queries) keep alpha, beta in registers even for the paper's 10-2k
+                             penalties (alpha 2, beta 12), which otherwise run instances with them as
+                             immediates (3.5 % / ~5 % faster; identical results) */
   int32_t reserved[2];    /* must be 0 */
 } sw_tuning;
 

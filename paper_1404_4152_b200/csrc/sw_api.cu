@@ -237,9 +237,25 @@ void* intra_kernel_nc(const IntraShape& sh) {
     default: return sh.smem ? (void*)swk::k_intra16<16, true, NC> : (void*)swk::k_intra16<16, false, NC>;
   }
 }
+// The production shape (4 columns per step, profile in shared memory) with the
+// paper's gap penalties as immediates (sw_common.cuh, kFixedAlpha/kFixedBeta).
+void* intra_kernel_fixed_gaps(int tr) {
+  switch (tr) {
+    case 4: return (void*)swk::k_intra16<4, true, 4, 1>;
+    case 5: return (void*)swk::k_intra16<5, true, 4, 1>;
+    case 6: return (void*)swk::k_intra16<6, true, 4, 1>;
+    case 7: return (void*)swk::k_intra16<7, true, 4, 1>;
+    case 8: return (void*)swk::k_intra16<8, true, 4, 1>;
+    case 10: return (void*)swk::k_intra16<10, true, 4, 1>;
+    case 12: return (void*)swk::k_intra16<12, true, 4, 1>;
+    case 14: return (void*)swk::k_intra16<14, true, 4, 1>;
+    default: return (void*)swk::k_intra16<16, true, 4, 1>;
+  }
+}
 // intra_cols: columns per wavefront step (4 = production; 2 = the previous
 // design, ablation build only)
-void* intra_kernel(const IntraShape& sh, int intra_cols) {
+void* intra_kernel(const IntraShape& sh, int intra_cols, bool fixed_gaps) {
+  if (fixed_gaps && sh.smem && (intra_cols == 0 || intra_cols == 4)) return intra_kernel_fixed_gaps(sh.tr);
 #ifdef SW_ABLATION
   if (intra_cols == 2) return intra_kernel_nc<2>(sh);
 #endif

@@ -604,7 +604,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-template <int TR, bool SMEM, int NC = 2>
+template <int TR, bool SMEM, int NC = 2, int GAPS = 0>
 __global__ void __launch_bounds__(kInterThreads, 1)
 k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
           const int* __restrict__ n_groups_dev, const int* __restrict__ pos_map, int cut,
@@ -632,7 +632,8 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   if (SMEM) load_profile_smem(sprof, gprof, stride);
   const int lane = threadIdx.x & 31;
   uint2* bnd = scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * scratch_cols * 32;
-  const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
+  const uint32_t na2 = GAPS == 1 ? pack2(-kFixedAlpha) : pack2(-alpha);    // GAPS: as in k_inter16
+  const uint32_t nb2 = GAPS == 1 ? pack2(-kFixedBeta) : pack2(-beta);
   // First items are dealt across the SMs (warp k of CTA b takes item k*gridDim.x + b),
   // so the longest pairs -- the wavefront's critical paths -- do not share an SM;
   // the rest come longest-first from the counter.

@@ -101,7 +101,7 @@ __global__ void k_profile_pair(const uint8_t* __restrict__ qa, int ma, const uin
 }
 
 // Items: half-groups (32 subjects, the lo or hi members of a 64-subject group), longest first.
-template <int T>
+template <int T, int GAPS = 0>
 __global__ void __launch_bounds__(kInterThreads, 1)
 k_multi16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups, int cut,
           const uint32_t* __restrict__ gprof2, int m_pad, int stride2, int alpha, int beta, int limit,
@@ -120,7 +120,8 @@ k_multi16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   const int lane = threadIdx.x & 31;
   const long long wslot = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   uint2* bnd = scratch + wslot * scratch_cols * 32;
-  const uint32_t na2 = pack2(-alpha), nb2 = pack2(-beta);
+  const uint32_t na2 = GAPS == 1 ? pack2(-kFixedAlpha) : pack2(-alpha);    // GAPS: as in k_inter16
+  const uint32_t nb2 = GAPS == 1 ? pack2(-kFixedBeta) : pack2(-beta);
   const int nfull = m_pad / T, rem = m_pad - nfull * T;
   const int n_items = 2 * n_groups;
   for (;;) {

@@ -67,13 +67,15 @@ def test_gap_parameters(alpha, beta):
     _check(db, _query(300, 2), B62, alpha, beta)
 
 
-@pytest.mark.parametrize("big", [False, True])
-def test_fixed_gap_instance_equals_generic(big):
-    """The paper's 10-2k penalties (alpha 2, beta 12) run a first-pass instance with
-    them as immediates; sw_tuning.generic_gaps = 1 forces the register instance.  Both
-    give the oracle's scores on tiles, ragged tails, wide groups (own slabs) and
-    planted copies past LIMIT16 (int32 reruns); neighbouring penalties take the
-    generic instance."""
+@pytest.mark.parametrize("path", ["auto", "inter_big", "intra"])
+def test_fixed_gap_instances_equal_generic(path):
+    """The paper's 10-2k penalties (alpha 2, beta 12) run first-pass instances (inter-task,
+    intra-task wavefront, paired queries) with them as immediates; sw_tuning.generic_gaps = 1
+    forces the register instances.  Both give the oracle's scores on tiles, ragged tails,
+    wide groups (own slabs), the wavefront and planted copies past LIMIT16 (int32 reruns);
+    neighbouring penalties take the generic instances."""
+    big = path == "inter_big"
+    lt = {"auto": 0, "inter_big": -1, "intra": 1}[path]
     rng = np.random.default_rng(4212 + big)
     lens = np.concatenate([rng.integers(0, 700, size=800), [6400, 6400, 0, 1]])
     if big:
@@ -84,11 +86,17 @@ def test_fixed_gap_instance_equals_generic(big):
     db.residues[db.offsets[801]:db.offsets[801] + 6400] = q[100:6500]
     for m in (100, 6600):
         for tuning in ({}, {"generic_gaps": 1}):
-            r = _check(db, q[:m], B62, 2, 12, k=6, long_threshold=-1 if big else 0, tuning=tuning)
+            r = _check(db, q[:m], B62, 2, 12, k=6, long_threshold=lt, tuning=tuning)
             if m == 6600:
                 assert r.stats["n_rerun32"] >= 1
-        _check(db, q[:m], B62, 2, 13, long_threshold=-1 if big else 0)
-        _check(db, q[:m], B62, 3, 12, long_threshold=-1 if big else 0)
+        _check(db, q[:m], B62, 2, 13, long_threshold=lt)
+        _check(db, q[:m], B62, 3, 12, long_threshold=lt)
+    qs = [q[:300], q[1000:1290]]                                             # paired into one int16x2 pass
+    for tuning in ({}, {"generic_gaps": 1}):
+        with sw.Database.from_synth(db, device=0, long_threshold=lt, tuning=tuning) as g:
+            r = g.search_batch(qs, B62, 2, 12, k=5)
+        for i, qq in enumerate(qs):
+            assert np.array_equal(r.scores[i], oracle.db_scores(qq, db, B62, 2, 12))
 
 
 def test_blosum50_and_random_asymmetric_matrices():

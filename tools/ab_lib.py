@@ -1,5 +1,5 @@
 """A/B: first-pass time with the in-tree library and an alternative build (path in argv[1]);
-AB_TUNING (JSON) passes sw_tuning fields, e.g. AB_TUNING='{"generic_gaps": 1}'."""
+AB_TUNING (JSON) passes sw_tuning fields, e.g. AB_TUNING='{"generic_gaps": 1}'; AB_LT sets long_threshold."""
 import json
 import os
 import sys
@@ -17,8 +17,9 @@ sdb = make_db(cfg)
 q = make_query(cfg)
 M = cfg.matrix32()
 tuning = json.loads(os.environ.get("AB_TUNING", "{}"))
-g = sw.Database.from_synth(sdb, device=0, tuning=tuning or None)
+g = sw.Database.from_synth(sdb, device=0, tuning=tuning or None, long_threshold=int(os.environ.get("AB_LT", "0")))
 for _ in range(3):
     g.search(q, M, cfg.alpha, cfg.beta, k=10)
-t = sorted(g.search(q, M, cfg.alpha, cfg.beta, k=10).stats["ms_inter"] for _ in range(6))
-print(os.path.basename(sw.LIB_PATH), tuning, cfg.name, "first pass ms min/median", round(t[0], 3), round(t[3], 3), flush=True)
+n = int(os.environ.get("AB_N", "6"))
+t = sorted(g.search(q, M, cfg.alpha, cfg.beta, k=10).stats["ms_inter"] for _ in range(n))
+print(os.path.basename(sw.LIB_PATH), tuning, cfg.name, "first pass ms min/median", round(t[0], 3), round(t[n // 2], 3), flush=True)

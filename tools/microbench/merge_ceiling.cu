@@ -8,6 +8,14 @@
 //           subject; D = VIADD2(VIADD2(Hprev, HI), LO): no alu op for the merge
 //   MODE 2  one 32-bit zext table, D = VIADD2(IMAD(T_hi, 0x10000, Hprev), T_lo)
 //   MODE 3+x mixed: rows (r % 8) < NP use MODE 0, the others MODE 1
+//   (round 2, second pass) biased int16 table u = s + beta >= 0 ([25][s16] u16,
+//   rows i, i+1 in one word), D = VIADD2(H(i-1) - beta, pair):
+//   MODE 5  PRMT per row (0x5410 / 0x7632), no sign replication needed
+//   MODE 6  even rows: pair = HFMA2(W_lo, (1.0, 0.0), W_hi << 16) (fma pipe: the
+//           fp16 multiply by 1 / 0 is exact on these subnormal bit patterns),
+//           odd rows: PRMT 0x7632
+//   MODE 7  every row on the fma pipe (odd rows: HFMA2(W_hi, (0.0, 1.0), W_lo >> 16))
+//   LW = 16 or 8: LDS.128 per 8 rows or LDS.64 per 4 rows per subject
 // Reports Gcell/s (2 cells per lane-row) at 384 threads / SM.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o merge_ceiling merge_ceiling.cu
 #include <cstdint>
@@ -17,6 +25,12 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r; asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel)); return r; }
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r; asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r; }
+__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r; asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r; }
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) {
+  uint32_t r; asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r; }
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 v; asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"((uint32_t)__cvta_generic_to_shared(p))); return v; }
 __device__ __forceinline__ uint2 lds64(const void* p) {
   uint2 v; asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"((uint32_t)__cvta_generic_to_shared(p))); return v; }
 __host__ __device__ constexpr uint32_t sel_pair(int rr) {
@@ -90,6 +104,78 @@ __global__ void __launch_bounds__(NT, 1) k(uint32_t* out, int ncols, int s8, int
   out[blockIdx.x * blockDim.x + threadIdx.x] = hmax ^ e;
 }
 
+// Biased int16 table variants (MODE 5..7).  s16 = row stride in u16 units (multiple of 8).
+template <int MODE, int LW, int R = 48, int NT = 384>
+__global__ void __launch_bounds__(NT, 1) k16(uint32_t* out, int ncols, int s16) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint16_t* t16 = (uint16_t*)sm;                              // [25][s16]
+  for (int t = threadIdx.x; t < 25 * s16; t += blockDim.x) {
+    const int r = t / s16, i = t % s16;
+    t16[t] = (uint16_t)(r == 24 ? 12 : (((r * 7 + i * 13) % 15) - 4) + 12);
+  }
+  __syncthreads();
+  uint32_t D[R], F[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) { D[r] = 0; F[r] = 0; }
+  uint32_t e = 0, hmax = 0;
+  const uint32_t na2 = 0xfffefffeu, nb2 = 0xfff4fff4u, one_lo = 0x00003c00u, one_hi = 0x3c000000u;
+  uint32_t w = 0x9e3779b9u * (threadIdx.x + 1 + blockIdx.x * 977);
+  const int i0 = R * (blockIdx.x % (M / R));
+  for (int j = 0; j < ncols; j++) {
+    w = w * 1664525u + 1013904223u;
+    const uint32_t rlo = ((w >> 24) * 25u) >> 8, rhi = (((w >> 16) & 255u) * 25u) >> 8;
+    const uint16_t* a16 = t16 + rlo * s16 + i0;
+    const uint16_t* b16 = t16 + rhi * s16 + i0;
+    uint32_t hbprev = e ^ (uint32_t)j, hodd = 0;
+    e = 0;
+    uint32_t A[LW / 4], B[LW / 4];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      constexpr int RPL = LW / 2;                            // rows per load
+      if (r % RPL == 0) {
+        if constexpr (LW == 16) {
+          const uint4 x = lds128(a16 + r), y = lds128(b16 + r);
+          A[0] = x.x; A[1] = x.y; A[2] = x.z; A[3] = x.w; B[0] = y.x; B[1] = y.y; B[2] = y.z; B[3] = y.w;
+        } else {
+          const uint2 x = lds64(a16 + r), y = lds64(b16 + r);
+          A[0] = x.x; A[1] = x.y; B[0] = y.x; B[1] = y.y;
+        }
+      }
+      const uint32_t wl = A[(r % RPL) / 2], wh = B[(r % RPL) / 2];
+      uint32_t pr;
+      if (MODE == 5) pr = prmt(wl, wh, (r & 1) ? 0x7632u : 0x5410u);
+      else if (!(r & 1)) pr = hfma2(wl, one_lo, imad(wh, 0x10000u, 0u));
+      else if (MODE == 6) pr = prmt(wl, wh, 0x7632u);
+      else pr = hfma2(wh, one_hi, mulhi(wl, 0x10000u));
+      const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);
+      D[r] = __vadd2(hbprev, pr);
+      const uint32_t hb = __vadd2(h, nb2);
+      e = __viaddmax_s16x2_relu(e, na2, hb);
+      F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+      if (r & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
+      else hodd = h;
+      hbprev = hb;
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = hmax ^ e;
+}
+
+template <int MODE, int LW, int R = 48, int NT = 384>
+void run16(const char* name, uint32_t* d_out, int nsm, int s16) {
+  const int ncols = 4096, threads = NT;
+  const size_t smem = 25 * (size_t)s16 * 2;
+  cudaFuncSetAttribute(k16<MODE, LW, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; rep++) {
+    cudaEventRecord(e0); k16<MODE, LW, R, NT><<<nsm, threads, smem>>>(d_out, ncols, s16); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); float ms; cudaEventElapsedTime(&ms, e0, e1); if (rep && ms < best) best = ms;
+  }
+  cudaError_t err = cudaGetLastError();
+  const double cells = 2.0 * R * ncols * threads * (double)nsm;
+  printf("%-34s R=%d NT=%d s16=%d LW=%d  %.1f Gcell/s %s\n", name, R, NT, s16, LW, cells / (best * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
+}
+
 template <int MODE, int NP = 0, int R = 48, int NT = 384>
 void run(const char* name, uint32_t* d_out, int nsm, int s32) {
   const int ncols = 4096, threads = NT;
@@ -109,6 +195,18 @@ void run(const char* name, uint32_t* d_out, int nsm, int s32) {
 int main() {
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   uint32_t* d_out; cudaMalloc(&d_out, 4 * nsm * 512);
+  if (getenv("INT16")) {
+    run<0>("mode0 int8+PRMT", d_out, nsm, M + 2);
+    for (int s16 : {M + 8, M + 16, M + 32, M + 64}) {
+      run16<5, 16>("mode5 int16 PRMT", d_out, nsm, s16);
+      run16<6, 16>("mode6 int16 HFMA2/PRMT", d_out, nsm, s16);
+      run16<7, 16>("mode7 int16 HFMA2 all", d_out, nsm, s16);
+      run16<5, 8>("mode5 int16 PRMT", d_out, nsm, s16);
+      run16<6, 8>("mode6 int16 HFMA2/PRMT", d_out, nsm, s16);
+      run16<7, 8>("mode7 int16 HFMA2 all", d_out, nsm, s16);
+    }
+    return 0;
+  }
   if (getenv("TILES")) {
     run<0, 0, 48, 384>("mode0", d_out, nsm, M + 2);
     run<0, 0, 32, 512>("mode0", d_out, nsm, M + 2);
