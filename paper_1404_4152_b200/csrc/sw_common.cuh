@@ -116,6 +116,31 @@ __global__ void k_profile(const uint8_t* __restrict__ q, int m, const int8_t* __
 }
 
 
+// Stage (i) of a search in one launch: the query profile, the blocked profile of
+// the intra-task wavefront (both as above) and the zeroing of the search's
+// work-queue counters (nz ints), which were two kernels and two memsets.
+__global__ void k_profiles(const uint8_t* __restrict__ q, int m, const int8_t* __restrict__ M,
+                           int8_t* __restrict__ prof, int stride, int8_t* __restrict__ profb, int tr, int nblk,
+                           int* __restrict__ zero_a, int nza, int* __restrict__ zero_b, int nzb) {
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  if (t0 < nza) zero_a[t0] = 0;
+  if (t0 < nzb) zero_b[t0] = 0;
+  const int total = kProfRows * stride;
+  for (int t = t0; t < total; t += nt) {
+    const int r = t / stride, i = t - r * stride;
+    int8_t v = 0;
+    if (i < m && r < kNumCodes) v = M[q[i] * 32 + r];
+    prof[t] = v;
+  }
+  const int row = nblk * 16, totb = kProfRows * row;
+  for (int t = t0; t < totb; t += nt) {
+    const int r = t / row, rem = t - r * row, b = rem >> 4, k = rem & 15, i = b * tr + k;
+    int8_t v = 0;
+    if (k < tr && i < m && r < kNumCodes) v = M[q[i] * 32 + r];
+    profb[t] = v;
+  }
+}
+
 struct ResCursor {
   uint2 w, wn;
   int c, wi, nwords;

@@ -68,6 +68,56 @@ __global__ void __launch_bounds__(kScanBlock) k_flag_scatter(const uint8_t* __re
   if (f) list[block_offsets[blockIdx.x] + warp_sums[w] + __popc(bal & ((1u << lane) - 1u))] = i;
 }
 
+// Small flag arrays (n <= kCompactBlockMax): count, scan and scatter in ONE CTA
+// instead of the three launches above.  Thread t owns the contiguous positions
+// [t*S, t*S + S), S = ceil(n / 1024) <= 64, read with independent loads (one
+// memory latency, not one per 1,024-flag chunk); one block scan of the per-thread
+// counts orders the list.  Same ascending list, total and tail-group count.
+constexpr int kCompactBlockMax = 65536;
+
+__global__ void __launch_bounds__(kScanBlock) k_flag_compact_block(const uint8_t* __restrict__ flag, int n,
+                                                                   int* __restrict__ list, int* __restrict__ total,
+                                                                   int* __restrict__ tail_groups) {
+  __shared__ int warp_sums[kScanBlock / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int S = (n + kScanBlock - 1) / kScanBlock;
+  const int p0 = t * S, p1 = min(n, p0 + S);
+  unsigned long long bits = 0ull;                  // bit j: position p0 + j is flagged (S <= 64)
+#pragma unroll 16
+  for (int p = p0; p < p1; p++)
+    if (flag[p]) bits |= 1ull << (p - p0);
+  const int c = __popcll(bits);
+  int incl = c;                                    // block exclusive scan of c
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_sums[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int x = warp_sums[lane];
+    int y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += v;
+    }
+    warp_sums[lane] = y - x;
+    if (lane == 31) {
+      if (total) *total = y;
+      if (tail_groups) *tail_groups = (y + kGroup - 1) / kGroup;
+    }
+  }
+  __syncthreads();
+  int o = warp_sums[w] + incl - c;
+  while (bits) {
+    const int j = __ffsll((long long)bits) - 1;
+    list[o++] = p0 + j;
+    bits &= bits - 1;
+  }
+}
+
 // mini-group sizes (words) of a sorted flagged list: ncols = length of the group's last member
 __global__ void k_mini_sizes(const int* __restrict__ list, const int* __restrict__ count_ptr,
                              const int* __restrict__ len_sorted, int n_mini_max, int* __restrict__ sizes) {

@@ -137,16 +137,59 @@ __global__ void __launch_bounds__(1024) k_topk_small(const unsigned long long* _
 // loads per thread (C1: 22 us per ranking before).
 constexpr int kTopkSmemKeys = 12288;              // 96 KB of dynamic shared memory
 
-__global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* __restrict__ gkeys, int n, int k,
-                                                     long long* __restrict__ out_ids, int* __restrict__ out_scores) {
-  extern __shared__ unsigned long long skeys[];
-  const bool staged = n <= kTopkSmemKeys;
-  if (staged) {
-#pragma unroll 4
-    for (int p = threadIdx.x; p < n; p += blockDim.x) skeys[p] = gkeys[p];
+// Small k (<= 32): k rounds of a block-wide argmax over the unique keys (the
+// owner of each round's winner rescans its keys below it); a few us for C1's
+// top-10 instead of eight radix passes (~17 us).
+// Warp max of 64-bit keys with two REDUX.MAX (high words, then the low words of
+// the lanes holding the highest high word) instead of a 10-SHFL butterfly.
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+  const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(v >> 32));
+  const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(v >> 32) == hi ? (unsigned)v : 0u);
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+__device__ __forceinline__ void topk_rounds(const unsigned long long* __restrict__ keys, int n, int k,
+                                            long long* __restrict__ out_ids, int* __restrict__ out_scores) {
+  __shared__ unsigned long long wbest[32], sel;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+  unsigned long long best = 0ull;                   // keys are >= 1 (ids <= 2^32 - 2): 0 = none
+  for (int p = t; p < n; p += blockDim.x) best = max(best, keys[p]);
+  const int cnt = min(k, n);
+  for (int r = 0; r < cnt; r++) {
+    const unsigned long long v = warp_max_u64(best);
+    if (lane == 0) wbest[w] = v;
     __syncthreads();
+    if (w == 0) {
+      const unsigned long long x = warp_max_u64(lane < nw ? wbest[lane] : 0ull);
+      if (lane == 0) {
+        sel = x;
+        if (out_ids) out_ids[r] = (long long)(0xffffffffull - (x & 0xffffffffull));
+        if (out_scores) out_scores[r] = (int)(x >> 32);
+      }
+    }
+    __syncthreads();
+    const unsigned long long s = sel;
+    if (best == s) {                                // the one thread holding it (unique keys)
+      best = 0ull;
+      for (int p = t; p < n; p += blockDim.x) {
+        const unsigned long long x = keys[p];
+        if (x < s && x > best) best = x;
+      }
+    }
   }
-  const unsigned long long* keys = staged ? skeys : gkeys;
+  for (int r = cnt + t; r < k; r += blockDim.x) {
+    if (out_ids) out_ids[r] = -1;
+    if (out_scores) out_scores[r] = -1;
+  }
+}
+
+// The whole ranking of n <= 65,536 keys (min(k, n) <= 4,096) by one CTA.
+__device__ __forceinline__ void topk_block_impl(const unsigned long long* __restrict__ keys, int n, int k,
+                                                long long* __restrict__ out_ids, int* __restrict__ out_scores) {
+  if (k <= 32) {
+    topk_rounds(keys, n, k, out_ids, out_scores);
+    return;
+  }
   __shared__ unsigned long long s[4096];
   __shared__ unsigned hist[256];
   __shared__ unsigned long long sh_prefix, sh_mask;
@@ -239,6 +282,53 @@ __global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* _
       if (out_scores) out_scores[t] = -1;
     }
   }
+}
+
+
+__global__ void __launch_bounds__(1024) k_topk_block(const unsigned long long* __restrict__ gkeys, int n, int k,
+                                                     long long* __restrict__ out_ids, int* __restrict__ out_scores) {
+  extern __shared__ unsigned long long skeys[];
+  const bool staged = n <= kTopkSmemKeys;
+  if (staged) {
+#pragma unroll 4
+    for (int p = threadIdx.x; p < n; p += blockDim.x) skeys[p] = gkeys[p];
+    __syncthreads();
+  }
+  topk_block_impl(staged ? skeys : gkeys, n, k, out_ids, out_scores);
+}
+
+// n <= kTopkSmemKeys: stage (iv) in ONE launch -- k_finalize's scatter and keys
+// (into shared memory) followed by the one-CTA top-k (C1: two launches less
+// per search than finalize + k_topk_block).
+__global__ void __launch_bounds__(1024) k_rank_block(const int* __restrict__ score_sorted, const int* __restrict__ perm,
+                                                     int n, const long long* __restrict__ gid,
+                                                     int* __restrict__ scores_out, int k,
+                                                     long long* __restrict__ out_ids, int* __restrict__ out_scores) {
+  extern __shared__ unsigned long long skeys[];
+  // n <= kTopkSmemKeys = 12 x 1024: a thread's loads go out four items at a
+  // time before their first use (one memory latency per four items)
+  for (int p0 = threadIdx.x; p0 < n; p0 += 4 * 1024) {
+    int idx[4], sc[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int p = p0 + u * 1024;
+      idx[u] = p < n ? perm[p] : 0;
+      sc[u] = p < n ? score_sorted[p] : 0;
+    }
+    unsigned long long id[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) id[u] = gid ? (unsigned long long)gid[idx[u]] : (unsigned long long)idx[u];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int p = p0 + u * 1024;
+      if (p < n) {
+        if (scores_out) scores_out[idx[u]] = sc[u];
+        skeys[p] = ((unsigned long long)(unsigned)sc[u] << 32) | (0xffffffffull - id[u]);
+      }
+    }
+  }
+  __syncthreads();
+  if (out_ids || out_scores) topk_block_impl(skeys, n, k, out_ids, out_scores);
 }
 
 __global__ void k_topk_decode(const unsigned long long* __restrict__ sorted, int cnt, int k,

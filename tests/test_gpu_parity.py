@@ -150,6 +150,44 @@ def test_escalation_chain_8_16_32_exact():
         assert r.stats["n_rerun32"] == int((ref > limit16).sum())
 
 
+@pytest.mark.parametrize("n", [1, 33, 12288, 12289, 65536, 65537])
+def test_ranking_paths_and_sizes(n):
+    """The ranking paths by database size: n <= 12,288 one fused launch (scatter +
+    keys in shared memory + top-k), n <= 65,536 one CTA over global keys, larger the
+    multi-CTA radix select; k <= 32 by block-wide argmax rounds, larger k by radix
+    select + bitonic sort.  Heavy score ties (4-letter alphabet, short subjects) with
+    permuted global ids: the top-k equals the oracle's (score desc, id asc) order."""
+    rng = np.random.default_rng(n)
+    db = random_db(700 + n % 97, rng.integers(0, 24, size=n), alphabet=4)
+    gids = rng.permutation(np.arange(3 * n, dtype=np.int64))[:n]
+    q = _query(17, 3)
+    ref = oracle.db_scores(q, db, B62, 2, 12)
+    with sw.Database(db.residues, db.offsets, db.lengths, global_ids=gids, device=0) as g:
+        for k in (1, 10, 32, 33, 100):
+            r = g.search(q, B62, 2, 12, k=k)
+            assert np.array_equal(r.scores, ref)
+            ti, ts = oracle.topk(ref, k, gids)
+            assert np.array_equal(r.topk_ids, ti) and np.array_equal(r.topk_scores, ts), k
+
+
+def test_rerun_compaction_above_one_cta():
+    """More than 65,536 subjects with int16-saturating planted copies scattered over
+    the sorted order: the multi-CTA flag compaction gives the same int32 reruns as the
+    one-CTA path (exact scores, exact rerun count)."""
+    rng = np.random.default_rng(65)
+    q = _query(6500, 65)
+    n = 70000
+    lens = rng.integers(1, 60, size=n)
+    hot = rng.choice(n, size=12, replace=False)
+    lens[hot] = 6400 + rng.integers(0, 100, size=hot.size)
+    db = random_db(65, lens)
+    for t in hot:
+        db.residues[db.offsets[t]:db.offsets[t] + 6400] = q[:6400]
+    r = _check(db, q, B62, 2, 12, k=20)
+    ref = oracle.db_scores(q, db, B62, 2, 12)
+    assert r.stats["n_rerun32"] == int((ref > 32767 - 11).sum()) == hot.size
+
+
 @pytest.mark.parametrize("tile_rows,threads", [(32, 0), (32, 384), (48, 0), (48, 512), (64, 0)])
 def test_tile_rows_invariance(tile_rows, threads):
     """Scores do not depend on the register-tile height or CTA size (SPEC.md:252-255,
