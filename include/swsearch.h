@@ -93,7 +93,10 @@ typedef struct sw_tuning {
                              paired queries) keep alpha, beta in registers even for the paper's 10-2k
                              penalties (alpha 2, beta 12), which otherwise run instances with them as
                              immediates (3.5 % / ~5 % faster; identical results) */
-  int32_t reserved[2];    /* must be 0 */
+  int32_t intra_chain;    /* intra-task kernel, single-pass queries (m <= 32 x rows per lane): 0 = the
+                             pair items of a warp run as one chained stream through the lanes (no fill
+                             and drain per item), -1 = one wavefront per item (measurement) */
+  int32_t reserved[1];    /* must be 0 */
 } sw_tuning;
 
 typedef struct sw_opts {

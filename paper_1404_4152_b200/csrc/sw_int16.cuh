@@ -537,6 +537,175 @@ __device__ __forceinline__ void wait_words_ready(const long long* ready_from, lo
   }
 }
 
+// Single-pass intra-task items chained through the lanes (m_pad <= 32*TR, NC
+// columns per step).  intra_multi16 fills and drains the lane wavefront for every
+// pair item: nact - 1 of its K + nact - 1 steps run with idle lanes (C1: ~25 % of
+// the steps).  Here lane 0 starts the next item at the step after it finished the
+// current one, while the lanes below still finish theirs: the warp runs one
+// stream of steps over consecutive items of the work queue.  Each step's control
+// word (item index, first / last step) travels down the lanes with the E/H and
+// residue values it belongs to; a lane resets its rows at an item's first step,
+// and at its last step passes max(own running max, the one from above) on, so
+// the last active lane holds the pair's score and emits it.  Items are claimed
+// (and their residues decoded, one step per lane) a block of 32 steps ahead.
+constexpr uint32_t kCtlVoid = 0xffffffffu, kCtlFirst = 1u << 29, kCtlLast = 1u << 30, kCtlItem = (1u << 29) - 1;
+
+template <int TR, bool SMEM, int NC>
+__device__ __forceinline__ void intra_chain16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
+                                              int n_groups, int n_items, int first_item, int n_warps,
+                                              int* __restrict__ counter, const int* __restrict__ len_sorted,
+                                              const long long* __restrict__ ready_from,
+                                              const int8_t* __restrict__ gprof, int stride, int m_pad,
+                                              uint32_t na2, uint32_t nb2, int limit, const int* __restrict__ pos_map,
+                                              int* __restrict__ score_sorted, uint8_t* __restrict__ flag, int lane) {
+  static_assert(NC == 4 || NC == 8, "columns per step");
+  constexpr int NR = NC / 2;
+  const int8_t* pr = prof_base<SMEM>(gprof) + lane * 16;
+  const int nact = min(32, (m_pad + TR - 1) / TR);
+  // ---- the item stream (warp-uniform): claimed in queue order, mapped to steps
+  int next_claim = first_item;              // the dealt first item, then the counter
+  int it = -1, itK = 0, itk = 0;            // item being mapped, its steps, next step to map
+  int it_ncols = 0, it_nwords = 0;
+  const uint2* it_pw = nullptr;
+  bool exhausted = false;
+  long long mapped = 0;                     // steps mapped so far (stream positions)
+  auto claim = [&]() {
+    for (;;) {
+      int x;
+      if (next_claim >= 0) {
+        x = next_claim;
+        next_claim = -1;
+      } else {
+        x = 0;
+        if (lane == 0) x = n_warps + atomicAdd(counter, 1);
+        x = __shfl_sync(0xffffffffu, x, 0);
+      }
+      if (x >= n_items) { exhausted = true; it = -1; return; }
+      const int g = n_groups - 1 - x / 32, p = 31 - x % 32;
+      const GroupDesc gd = groups[g];
+      if (2 * p >= gd.count) continue;
+      wait_words_ready(ready_from, gd.base);
+      it = x;
+      it_ncols = len_sorted ? len_sorted[(long long)g * kGroup + min(2 * p + 1, gd.count - 1)] : gd.ncols;
+      it_nwords = (it_ncols + kResPerWord - 1) / kResPerWord;
+      it_pw = words + gd.base + p;
+      itK = (it_ncols + NC) / NC;
+      itk = 0;
+      return;
+    }
+  };
+  // descriptors of the next 32 stream positions: lane t gets position base + t
+  auto gen = [&](uint32_t (&rp)[NR], uint32_t& ctl) {
+    ctl = kCtlVoid;
+#pragma unroll
+    for (int i = 0; i < NR; i++) rp[i] = 0u;
+    int t0 = 0;
+    while (t0 < 32) {
+      if (it < 0 || itk >= itK) {
+        if (exhausted) break;
+        claim();
+        if (it < 0) break;
+      }
+      const int take = min(32 - t0, itK - itk);
+      if (lane >= t0 && lane < t0 + take) {
+        const int k = itk + lane - t0;
+#pragma unroll
+        for (int i = 0; i < NR; i++) {
+          const int c0 = NC * k + 2 * i, c1 = c0 + 1;
+          const uint2 w0 = res_word(it_pw, c0, it_nwords), w1 = res_word(it_pw, c1, it_nwords);
+          const int s0 = res_shift(c0), s1 = res_shift(c1);
+          rp[i] = ((w0.x >> s0) & 31u) | (((w0.y >> s0) & 31u) << 5) | (((w1.x >> s1) & 31u) << 10) |
+                  (((w1.y >> s1) & 31u) << 15);
+        }
+        ctl = (uint32_t)it | (k == 0 ? kCtlFirst : 0u) | (k == itK - 1 ? kCtlLast : 0u);
+      }
+      t0 += take;
+      itk += take;
+      mapped += take;
+    }
+  };
+  uint32_t D[TR], F[TR];
+#pragma unroll
+  for (int r = 0; r < TR; r++) { D[r] = 0u; F[r] = 0u; }
+  uint32_t hmax = 0u, hm_out = 0u, ctl_out = kCtlVoid;
+  uint32_t e_out[NC], h_out[NC], r_out[NR];
+#pragma unroll
+  for (int c = 0; c < NC; c++) { e_out[c] = 0u; h_out[c] = 0u; }
+#pragma unroll
+  for (int i = 0; i < NR; i++) r_out[i] = 0u;
+  uint32_t rp_cur[NR], rp_nxt[NR], ctl_cur, ctl_nxt;
+  gen(rp_cur, ctl_cur);
+  gen(rp_nxt, ctl_nxt);
+  for (long long sb = 0;; sb += 32) {
+    // every mapped position has passed the last active lane: done
+    if (exhausted && sb >= mapped + nact - 1) break;
+#pragma unroll 1
+    for (int t = 0; t < 32; t++) {
+      uint32_t e[NC], hp[NC], r_in[NR];
+#pragma unroll
+      for (int c = 0; c < NC; c++) {
+        e[c] = __shfl_up_sync(0xffffffffu, e_out[c], 1);
+        hp[c] = __shfl_up_sync(0xffffffffu, h_out[c], 1);
+      }
+#pragma unroll
+      for (int i = 0; i < NR; i++) r_in[i] = __shfl_up_sync(0xffffffffu, r_out[i], 1);
+      uint32_t ctl = __shfl_up_sync(0xffffffffu, ctl_out, 1);
+      uint32_t hm_in = __shfl_up_sync(0xffffffffu, hm_out, 1);
+#pragma unroll
+      for (int i = 0; i < NR; i++) {
+        const uint32_t v = __shfl_sync(0xffffffffu, rp_cur[i], t);
+        if (lane == 0) r_in[i] = v;
+      }
+      {
+        const uint32_t v = __shfl_sync(0xffffffffu, ctl_cur, t);
+        if (lane == 0) {
+          ctl = v;
+          hm_in = 0u;
+#pragma unroll
+          for (int c = 0; c < NC; c++) { e[c] = 0u; hp[c] = 0u; }   // E(0, col) = H(-1, col) = 0
+        }
+      }
+      if (lane < nact && ctl != kCtlVoid) {
+        if (ctl & kCtlFirst) {
+#pragma unroll
+          for (int r = 0; r < TR; r++) { D[r] = 0u; F[r] = 0u; }
+          hmax = 0u;
+        }
+        uint4 pa[NC], pb[NC];
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+          const uint32_t rr = r_in[c >> 1] >> (10 * (c & 1));
+          pa[c] = *reinterpret_cast<const uint4*>(pr + (rr & 31u) * stride);
+          pb[c] = *reinterpret_cast<const uint4*>(pr + ((rr >> 5) & 31u) * stride);
+        }
+        col16b_xn<TR, NC>(D, F, e, hp, pa, pb, na2, nb2, hmax);
+        if (ctl & kCtlLast) {
+          const uint32_t hm = __vmaxs2(hmax, hm_in);
+          if (lane == nact - 1) {
+            const int x = (int)(ctl & kCtlItem);
+            const int g = n_groups - 1 - x / 32, p = 31 - x % 32;
+            emit_pair(hm, g, 2 * p, groups[g].count, limit, pos_map, score_sorted, flag);
+          } else {
+            hm_out = hm;
+          }
+        }
+      } else {
+        ctl = kCtlVoid;
+      }
+#pragma unroll
+      for (int c = 0; c < NC; c++) { e_out[c] = e[c]; h_out[c] = hp[c]; }
+#pragma unroll
+      for (int i = 0; i < NR; i++) r_out[i] = r_in[i];
+      ctl_out = ctl;
+    }
+#pragma unroll
+    for (int i = 0; i < NR; i++) rp_cur[i] = rp_nxt[i];
+    ctl_cur = ctl_nxt;
+    gen(rp_nxt, ctl_nxt);
+  }
+  __syncwarp();
+}
+
 template <int T, bool SMEM, int NT, bool BIG = false, bool STATIC = false, int GAPS = 0>
 __global__ void __launch_bounds__(NT, 1)
 k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups, int n_groups,
@@ -615,7 +784,9 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
           const int8_t* __restrict__ gprof, int m_pad, int stride, int alpha, int beta, int limit,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
           int* __restrict__ score_sorted, uint8_t* __restrict__ flag, const int* __restrict__ len_sorted,
-          const long long* __restrict__ ready_from, int isolate) {
+          const long long* __restrict__ ready_from, int mode) {
+  // mode bit 0: isolate the warps holding the longest pairs; bit 1: no chained stream
+  const bool isolate = mode & 1, chain_off = mode & 2;
   // The inter-task kernel may start beside this one (programmatic dependent
   // launch): it only reads what was complete before this grid started.
   asm volatile("griddepcontrol.launch_dependents;");
@@ -653,6 +824,16 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   const int nw_active = isolate ? nw - (nw > 4) - (nw > 8) : nw;
   const int n_warps = gridDim.x * nw_active;
   int item = idle ? n_items : w_active * gridDim.x + blockIdx.x;
+  // single-pass queries (m up to 32 * TR rows): the items of a warp run as one
+  // chained stream (intra_chain16); the isolated critical warps keep the
+  // per-item wavefront with 8 columns per step
+  if constexpr (NC == 4) {
+    if (m_pad <= 32 * TR && !(isolate && w == 0) && !chain_off && !idle) {
+      intra_chain16<TR, SMEM, 4>(words, groups, n_groups, n_items, item, n_warps, counter, len_sorted, ready_from,
+                                 gprof, stride, m_pad, na2, nb2, limit, pos_map, score_sorted, flag, lane);
+      item = n_items;
+    }
+  }
   for (;; item = -1) {
     if (item < 0) {
       if (lane == 0) item = n_warps + atomicAdd(counter, 1);

@@ -60,6 +60,21 @@ def test_intra_wavefront_pass_boundaries(m):
     _check(random_db(2000 + m, lens), _query(m, 2), B62, 2, 12, long_threshold=1)
 
 
+@pytest.mark.parametrize("m", [1, 8, 100, 144, 300, 512])
+@pytest.mark.parametrize("tuning", [{}, {"intra_chain": -1}, {"intra_isolate": 1}, {"intra_isolate": -1}])
+def test_chained_intra_stream(m, tuning):
+    """Single-pass queries: a warp's pair items run as one chained stream through the
+    lanes (items of 1..60 steps, i.e. shorter and longer than the lane lag, empty
+    slots of partial groups, the last pairs of the queue).  Chained, per-item
+    (intra_chain -1) and isolated-warp runs all give the oracle's scores."""
+    rng = np.random.default_rng(31 + m)
+    lens = np.concatenate([rng.integers(0, 12, size=300), rng.integers(0, 240, size=700),
+                           rng.integers(200, 900, size=60), [0, 1, 2, 3, 5]])
+    rng.shuffle(lens)
+    db = random_db(3100 + m, lens)
+    _check(db, _query(m, 31), B62, 2, 12, k=12, long_threshold=1, tuning=tuning)
+
+
 @pytest.mark.parametrize("alpha,beta", [(0, 0), (1, 1), (2, 12), (1, 12), (5, 40), (0, 30), (3, 32767)])
 def test_gap_parameters(alpha, beta):
     rng = np.random.default_rng(alpha * 100 + beta)
