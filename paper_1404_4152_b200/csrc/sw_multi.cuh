@@ -56,12 +56,14 @@ __device__ __forceinline__ void tileq(const uint32_t* __restrict__ wp, int nword
   for (; j + 1 < ncols; j += 2) {
     const int shA = res_shift(j + 1), shB = res_shift(j + 2);
     uint32_t eA = bE.x, eB = bO.x;
-    const uint32_t hlA = colq<R>(D, F, eA, bE.y, pr + ((wA >> shA) & 31u) * stride2, na2, nb2, hmax);
-    const uint32_t hlB = colq<R>(D, F, eB, bO.y, pr + ((wB >> shB) & 31u) * stride2, na2, nb2, hmax);
-    wA = res_word32(wp, j + 3, nwords);
-    wB = res_word32(wp, j + 4, nwords);
+    const uint32_t tA = bE.y, tB = bO.y;
+    // next pair's tile-edge rows requested as soon as these are consumed (as in tile16)
     if (!first && j + 2 < ncols) bE = bnd[(j + 2) * 32 + lane];
     if (!first && j + 3 < ncols) bO = bnd[(j + 3) * 32 + lane];
+    const uint32_t hlA = colq<R>(D, F, eA, tA, pr + ((wA >> shA) & 31u) * stride2, na2, nb2, hmax);
+    const uint32_t hlB = colq<R>(D, F, eB, tB, pr + ((wB >> shB) & 31u) * stride2, na2, nb2, hmax);
+    wA = res_word32(wp, j + 3, nwords);
+    wB = res_word32(wp, j + 4, nwords);
     if (!last) {
       bnd[j * 32 + lane] = make_uint2(eA, hlA);
       bnd[(j + 1) * 32 + lane] = make_uint2(eB, hlB);
