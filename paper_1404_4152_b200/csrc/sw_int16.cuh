@@ -825,11 +825,13 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   const int n_warps = gridDim.x * nw_active;
   int item = idle ? n_items : w_active * gridDim.x + blockIdx.x;
   // single-pass queries (m up to 32 * TR rows): the items of a warp run as one
-  // chained stream (intra_chain16); the isolated critical warps keep the
-  // per-item wavefront with 8 columns per step
+  // chained stream (intra_chain16, 8 columns per step); the isolated critical
+  // warps keep the per-item wavefront with 8 columns per step
   if constexpr (NC == 4) {
     if (m_pad <= 32 * TR && !(isolate && w == 0) && !chain_off && !idle) {
-      intra_chain16<TR, SMEM, 4>(words, groups, n_groups, n_items, item, n_warps, counter, len_sorted, ready_from,
+      // 8 columns per step: with no fill and drain per item the longer step only
+      // amortises its shuffles and loads better (all-intra C2 27.8 -> 26.9 ms)
+      intra_chain16<TR, SMEM, 8>(words, groups, n_groups, n_items, item, n_warps, counter, len_sorted, ready_from,
                                  gprof, stride, m_pad, na2, nb2, limit, pos_map, score_sorted, flag, lane);
       item = n_items;
     }

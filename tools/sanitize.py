@@ -28,7 +28,7 @@ lens = np.concatenate([rng.integers(0, 400, size=700), [1, 2, 6, 7, 64, 65, 2500
 db = random_db(7, lens)
 q = gen_residues(stream_key(7, "sanitize-query", 200), 0, 200)
 ref = oracle.db_scores(q, db, M, 2, 12)
-cases = a.case.split(",") if a.case != "all" else ["search", "stream", "batch", "align", "pipeline"]
+cases = a.case.split(",") if a.case != "all" else ["search", "intra", "stream", "batch", "align", "pipeline"]
 
 
 def check(name, scores, want=ref):
@@ -50,6 +50,12 @@ if "search" in cases:
         r = g.search(ql, big, 2, 12, k=10)
     print("int32 reruns:", r.stats["n_rerun32"])
     check("search saturating", r.scores, oracle.db_scores(ql, db, big, 2, 12))
+if "intra" in cases:   # every long group pair-wise: chained streams, isolated warps, 10-2k and register instances
+    for tuning in ({}, {"intra_isolate": 1}, {"intra_chain": -1}, {"generic_gaps": 1}):
+        with sw.Database(db.residues, db.offsets, db.lengths, device=0, long_threshold=1, tuning=tuning) as g:
+            check(f"search all-intra {tuning}", g.search(q, M, 2, 12, k=10).scores)
+    with sw.Database(db.residues, db.offsets, db.lengths, device=0, long_threshold=1) as g:
+        check("search all-intra k=40 (radix top-k)", g.search(q, M, 2, 12, k=40).scores)
 if "stream" in cases:
     with sw.Database(db.residues, db.offsets, db.lengths, device=0, residency=1, chunk_mb=1) as g:
         check("search streamed", g.search(q, M, 2, 12, k=10).scores)
