@@ -96,6 +96,10 @@ typedef struct sw_tuning {
   int32_t intra_chain;    /* intra-task kernel, single-pass queries (m <= 32 x rows per lane): 0 = the
                              pair items of a warp run as one chained stream through the lanes (no fill
                              and drain per item), -1 = one wavefront per item (measurement) */
+  int32_t intra_split;    /* with intra_isolate in effect and a single-pass query: 0 = the longest pair of
+                             each isolated sub-partition (>= 1,024 columns) is cut into two column segments,
+                             the second run speculatively by a second warp and repaired at its start;
+                             -1 = one warp per pair (measurement) */
   int32_t reserved[1];    /* must be 0 */
 } sw_tuning;
 

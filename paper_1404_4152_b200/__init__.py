@@ -37,7 +37,8 @@ class sw_tuning(ctypes.Structure):
                 ("intra_cols", ctypes.c_int32), ("max_big", ctypes.c_int32), ("align_ws_kb", ctypes.c_int32),
                 ("pipeline", ctypes.c_int32), ("pipe_chain", ctypes.c_int32),
                 ("intra_isolate", ctypes.c_int32), ("generic_gaps", ctypes.c_int32),
-                ("intra_chain", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
+                ("intra_chain", ctypes.c_int32), ("intra_split", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 1)]
 
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)

@@ -537,6 +537,133 @@ __device__ __forceinline__ void wait_words_ready(const long long* ready_from, lo
   }
 }
 
+// Column segments of ONE pair for the latency-critical longest pairs (single
+// pass, NC columns per step): step k covers columns c0 + NC*k - 1 .. c0 + NC*k
+// + NC - 2 (column c0 - 1 primes the diagonal terms, as column -1 does in
+// intra_multi16).
+//   mode 0: from the zero state (the pair's first segment, c0 = 0); the lanes'
+//           final rows (D, F) go to `state` (2*TR words per lane, [r][lane]).
+//   mode 1: speculative -- from a zero left boundary (H(., c0 - 1) = 0); every
+//           kCkSteps steps each lane stores its rows in `ckpt`.
+//   mode 2: fix-up -- from the true rows in `state` (the previous segment's
+//           end); at every checkpoint each lane compares its rows with the
+//           speculative ones, the verdict is AND-ed down the lanes, and once the
+//           last lane sees all rows equal, every later column is the
+//           speculative run's and the pass stops.
+// Eq. 1 is monotone in its left boundary, so the speculative cells are lower
+// bounds of the true ones: the segment's maximum is max(speculative, fix-up).
+constexpr int kCkSteps = 16;
+constexpr int kSplitMinCols = 1024;   // shorter critical pairs run whole on warp 0
+
+template <int TR, bool SMEM, int NC>
+__device__ __forceinline__ uint32_t intra_seg16(const uint2* __restrict__ pw, int ncols, int c0, int K,
+                                                const int8_t* __restrict__ gprof, int stride, int m_pad,
+                                                uint32_t na2, uint32_t nb2, int lane, int mode,
+                                                uint32_t* __restrict__ ckpt, uint32_t* __restrict__ state) {
+  constexpr int NR = NC / 2;
+  const int8_t* pr = prof_base<SMEM>(gprof) + lane * 16;
+  const int nwords = (ncols + kResPerWord - 1) / kResPerWord;
+  const int nact = min(32, (m_pad + TR - 1) / TR);
+  uint32_t D[TR], F[TR];
+#pragma unroll
+  for (int r = 0; r < TR; r++) {
+    D[r] = mode == 2 ? state[r * 32 + lane] : 0u;
+    F[r] = mode == 2 ? state[(TR + r) * 32 + lane] : 0u;
+  }
+  uint32_t hmax = 0u, e_out[NC], h_out[NC], r_out[NR], f_out = 1u;
+#pragma unroll
+  for (int c = 0; c < NC; c++) { e_out[c] = 0u; h_out[c] = 0u; }
+#pragma unroll
+  for (int i = 0; i < NR; i++) r_out[i] = 0u;
+  auto fetch = [&](int kb, uint32_t (&rp)[NR]) {
+    const int k = kb + lane;
+#pragma unroll
+    for (int i = 0; i < NR; i++) {
+      const int a = c0 + NC * k + 2 * i, b = a + 1;
+      const uint2 w0 = res_word(pw, a, nwords), w1 = res_word(pw, b, nwords);
+      const int s0 = res_shift(a), s1 = res_shift(b);
+      rp[i] = ((w0.x >> s0) & 31u) | (((w0.y >> s0) & 31u) << 5) | (((w1.x >> s1) & 31u) << 10) |
+              (((w1.y >> s1) & 31u) << 15);
+    }
+  };
+  const int nsteps = K + nact - 1;
+  uint32_t rp_cur[NR], rp_nxt[NR];
+  fetch(0, rp_cur);
+  fetch(32, rp_nxt);
+  bool done = false;
+  for (int sb = 0; sb < nsteps && !done; sb += 32) {
+#pragma unroll 1
+    for (int t = 0; t < 32; t++) {
+      const int s = sb + t;
+      if (s >= nsteps) break;
+      uint32_t e[NC], hp[NC], r_in[NR];
+#pragma unroll
+      for (int c = 0; c < NC; c++) {
+        e[c] = __shfl_up_sync(0xffffffffu, e_out[c], 1);
+        hp[c] = __shfl_up_sync(0xffffffffu, h_out[c], 1);
+      }
+#pragma unroll
+      for (int i = 0; i < NR; i++) r_in[i] = __shfl_up_sync(0xffffffffu, r_out[i], 1);
+      uint32_t f_in = __shfl_up_sync(0xffffffffu, f_out, 1);
+#pragma unroll
+      for (int i = 0; i < NR; i++) {
+        const uint32_t v = __shfl_sync(0xffffffffu, rp_cur[i], t);
+        if (lane == 0) r_in[i] = v;
+      }
+      if (lane == 0) {
+        f_in = 1u;
+#pragma unroll
+        for (int c = 0; c < NC; c++) { e[c] = 0u; hp[c] = 0u; }      // E(0, col) = H(-1, col) = 0
+      }
+      const int k = s - lane;
+      uint32_t conv = 0u;
+      if (lane < nact && k >= 0 && k < K) {
+        uint4 pa[NC], pb[NC];
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+          const uint32_t rr = r_in[c >> 1] >> (10 * (c & 1));
+          pa[c] = *reinterpret_cast<const uint4*>(pr + (rr & 31u) * stride);
+          pb[c] = *reinterpret_cast<const uint4*>(pr + ((rr >> 5) & 31u) * stride);
+        }
+        col16b_xn<TR, NC>(D, F, e, hp, pa, pb, na2, nb2, hmax);
+        if (mode != 0 && (k % kCkSteps) == kCkSteps - 1) {
+          uint32_t* ck = ckpt + (long long)(k / kCkSteps) * (2 * TR * 32);
+          if (mode == 1) {
+#pragma unroll
+            for (int r = 0; r < TR; r++) { ck[r * 32 + lane] = D[r]; ck[(TR + r) * 32 + lane] = F[r]; }
+          } else {
+            bool eq = f_in != 0u;
+#pragma unroll
+            for (int r = 0; r < TR; r++) eq = eq && ck[r * 32 + lane] == D[r] && ck[(TR + r) * 32 + lane] == F[r];
+            f_in = eq ? 1u : 0u;
+            conv = (eq && lane == nact - 1) ? 1u : 0u;
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NC; c++) { e_out[c] = e[c]; h_out[c] = hp[c]; }
+#pragma unroll
+      for (int i = 0; i < NR; i++) r_out[i] = r_in[i];
+      f_out = f_in;
+      if (mode == 2 && __shfl_sync(0xffffffffu, conv, nact - 1)) {   // all rows equal: the rest is speculative's
+        done = true;
+        break;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NR; i++) rp_cur[i] = rp_nxt[i];
+    fetch(sb + 64, rp_nxt);
+  }
+  if (mode == 0) {
+#pragma unroll
+    for (int r = 0; r < TR; r++) { state[r * 32 + lane] = D[r]; state[(TR + r) * 32 + lane] = F[r]; }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hmax = __vmaxs2(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+  return hmax;
+}
+
 // Single-pass intra-task items chained through the lanes (m_pad <= 32*TR, NC
 // columns per step).  intra_multi16 fills and drains the lane wavefront for every
 // pair item: nact - 1 of its K + nact - 1 steps run with idle lanes (C1: ~25 % of
@@ -786,7 +913,7 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
           int* __restrict__ score_sorted, uint8_t* __restrict__ flag, const int* __restrict__ len_sorted,
           const long long* __restrict__ ready_from, int mode) {
   // mode bit 0: isolate the warps holding the longest pairs; bit 1: no chained stream
-  const bool isolate = mode & 1, chain_off = mode & 2;
+  const bool isolate = mode & 1, chain_off = mode & 2, split_off = mode & 4;
   // The inter-task kernel may start beside this one (programmatic dependent
   // launch): it only reads what was complete before this grid started.
   asm volatile("griddepcontrol.launch_dependents;");
@@ -824,11 +951,64 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   const int nw_active = isolate ? nw - (nw > 4) - (nw > 8) : nw;
   const int n_warps = gridDim.x * nw_active;
   int item = idle ? n_items : w_active * gridDim.x + blockIdx.x;
+  bool finished = idle;                                // takes no (more) items
+  // Isolated sub-partition, single-pass query: the longest pair dealt to warp 0
+  // is cut into two column segments (about half each): warp 0 runs the first,
+  // warp 4 (otherwise idle) the second speculatively from a zero boundary, then
+  // repairs its start from warp 0's final rows until they meet the speculative
+  // ones (intra_seg16).  Both warps share the sub-partition's issue slots, which
+  // the lone latency-bound wavefront leaves half empty.
+  if constexpr (NC == 4) {
+    if (isolate && (w == 0 || w == 4) && m_pad <= 32 * TR && !split_off) {
+      __shared__ uint32_t s_state[2 * 16 * 32 + 1];
+      const int it0 = blockIdx.x;                         // warp 0's dealt first item
+      int ncols0 = 0, g0 = 0, p0 = 0, cnt0 = 0;
+      const uint2* pw0 = nullptr;
+      if (it0 < n_items) {
+        g0 = n_groups - 1 - it0 / 32;
+        p0 = 31 - it0 % 32;
+        const GroupDesc gd = groups[g0];
+        cnt0 = gd.count;
+        if (2 * p0 < gd.count) {
+          ncols0 = len_sorted ? len_sorted[(long long)g0 * kGroup + min(2 * p0 + 1, gd.count - 1)] : gd.ncols;
+          pw0 = words + gd.base + p0;
+        }
+      }
+      const int c1 = ((ncols0 + 64) / 2 + 7) & ~7;                       // warp 0: columns [0, c1 - 1)
+      const int K0 = c1 / 8, K1 = (ncols0 + 1 - c1 + 7) / 8;
+      const long long ck_words = (long long)(K1 / kCkSteps + 1) * 2 * TR * 32;
+      const long long cap_words = scratch_cols * 32 * 2;                  // warp 4's slab, in 32-bit words
+      if (ncols0 >= kSplitMinCols && ck_words <= cap_words) {
+        uint32_t* ck = reinterpret_cast<uint32_t*>(scratch + ((long long)blockIdx.x * (blockDim.x >> 5) + 4) *
+                                                   scratch_cols * 32);
+        wait_words_ready(ready_from, groups[g0].base);
+        if (w == 0) {
+          const uint32_t h0 = intra_seg16<TR, SMEM, 8>(pw0, ncols0, 0, K0, gprof, stride, m_pad, na2, nb2, lane, 0,
+                                                      nullptr, s_state);
+          if (lane == 0) s_state[2 * 16 * 32] = h0;
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          item = -1;                                      // on to the queue
+        } else {
+          const uint32_t h1 = intra_seg16<TR, SMEM, 8>(pw0, ncols0, c1, K1, gprof, stride, m_pad, na2, nb2, lane, 1,
+                                                      ck, nullptr);
+          __threadfence_block();
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          const uint32_t h2 = intra_seg16<TR, SMEM, 8>(pw0, ncols0, c1, K1, gprof, stride, m_pad, na2, nb2, lane, 2,
+                                                      ck, s_state);
+          if (lane == 0)
+            emit_pair(__vmaxs2(__vmaxs2(h1, h2), s_state[2 * 16 * 32]), g0, 2 * p0, cnt0, limit, pos_map,
+                      score_sorted, flag);
+          item = n_items;                                 // warp 4 takes no other item
+          finished = true;
+        }
+      }
+    }
+  }
   // single-pass queries (m up to 32 * TR rows): the items of a warp run as one
   // chained stream (intra_chain16, 8 columns per step); the isolated critical
   // warps keep the per-item wavefront with 8 columns per step
   if constexpr (NC == 4) {
-    if (m_pad <= 32 * TR && !(isolate && w == 0) && !chain_off && !idle) {
+    if (m_pad <= 32 * TR && !(isolate && w == 0) && !chain_off && !finished) {
       // 8 columns per step: with no fill and drain per item the longer step only
       // amortises its shuffles and loads better (all-intra C2 27.8 -> 26.9 ms)
       intra_chain16<TR, SMEM, 8>(words, groups, n_groups, n_items, item, n_warps, counter, len_sorted, ready_from,

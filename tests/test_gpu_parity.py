@@ -75,6 +75,29 @@ def test_chained_intra_stream(m, tuning):
     _check(db, _query(m, 31), B62, 2, 12, k=12, long_threshold=1, tuning=tuning)
 
 
+@pytest.mark.parametrize("m", [40, 144, 300, 512])
+@pytest.mark.parametrize("tuning", [{"intra_isolate": 1}, {"intra_isolate": 1, "intra_split": -1}])
+def test_split_critical_pairs(m, tuning):
+    """The isolated warps' longest pairs (>= 1,024 columns) are cut into two column
+    segments, the second run speculatively from a zero boundary and repaired from
+    the first's final rows.  Random pairs (the repair meets the speculative rows
+    within a checkpoint or two), planted query copies straddling the cut (it meets
+    them only past the copy) and a long run of copies (it never meets them before
+    the end): every score equals the oracle's, with and without the split."""
+    rng = np.random.default_rng(700 + m)
+    q = _query(m, 70)
+    lens = np.concatenate([rng.integers(1024, 3200, size=70), rng.integers(0, 300, size=400)])
+    db = random_db(7000 + m, lens)
+    for t in range(0, 20, 3):                    # copies around the middle of the pair's columns
+        n = int(lens[t])
+        at = max(0, min(n - m, (n + 64) // 2 - m // 2 + int(rng.integers(-40, 40))))
+        db.residues[db.offsets[t] + at:db.offsets[t] + at + min(m, n)] = q[:min(m, n - at)]
+    n = int(lens[1])
+    for at in range(0, n - m, m):                # back-to-back copies over the whole subject
+        db.residues[db.offsets[1] + at:db.offsets[1] + at + m] = q
+    _check(db, q, B62, 2, 12, k=15, long_threshold=1, tuning=tuning)
+
+
 @pytest.mark.parametrize("alpha,beta", [(0, 0), (1, 1), (2, 12), (1, 12), (5, 40), (0, 30), (3, 32767)])
 def test_gap_parameters(alpha, beta):
     rng = np.random.default_rng(alpha * 100 + beta)
