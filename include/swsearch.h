@@ -100,7 +100,12 @@ typedef struct sw_tuning {
                              each isolated sub-partition (>= 1,024 columns) is cut into two column segments,
                              the second run speculatively by a second warp and repaired at its start;
                              -1 = one warp per pair (measurement) */
-  int32_t reserved[1];    /* must be 0 */
+  int32_t launch_chain;   /* resident databases: 0 = launch latency hidden behind the kernel before --
+                             up to 262,144 subjects the profile kernel also zeroes the saturation flags
+                             and the intra-task pass is launched as its programmatic dependent; up to
+                             65,536 the one-CTA flag compaction, the int32 rerun and the one-CTA ranking
+                             each follow the kernel before them the same way; -1 = plain stream-ordered
+                             launches (measurement).  Results never depend on it. */
 } sw_tuning;
 
 typedef struct sw_opts {

@@ -38,7 +38,7 @@ class sw_tuning(ctypes.Structure):
                 ("pipeline", ctypes.c_int32), ("pipe_chain", ctypes.c_int32),
                 ("intra_isolate", ctypes.c_int32), ("generic_gaps", ctypes.c_int32),
                 ("intra_chain", ctypes.c_int32), ("intra_split", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 1)]
+                ("launch_chain", ctypes.c_int32)]
 
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)

@@ -169,6 +169,7 @@ inline void* inter16_select(int T, int nt, bool smem, bool big, bool static_sche
   return inter16_kernel<48, 384>(smem, big);
 }
 constexpr int kMaxSmemProfile = 200 * 1024;
+constexpr int64_t kFlagZeroInProfiles = 1 << 18;   // databases up to this many subjects: flags zeroed by k_profiles
 constexpr size_t kSmemOptin = 227 * 1024 - 4096;  // B200 shared memory per block minus the kernels' static smem
 
 // Ring slots per link of the pipelined first pass for a profile of prof_bytes
@@ -356,6 +357,8 @@ struct sw_db {
   // per-search buffers
   uint8_t* d_query = nullptr;
   size_t query_cap = 0;
+  uint8_t* d_qm = nullptr;      // sw_search's matrix (1,024 B) and query behind it: one H2D copy per search
+  size_t qm_cap = 0;
   int8_t* d_matrix = nullptr;
   int8_t* d_prof = nullptr;
   size_t prof_cap = 0;

@@ -121,10 +121,12 @@ __global__ void k_profile(const uint8_t* __restrict__ q, int m, const int8_t* __
 // work-queue counters (nz ints), which were two kernels and two memsets.
 __global__ void k_profiles(const uint8_t* __restrict__ q, int m, const int8_t* __restrict__ M,
                            int8_t* __restrict__ prof, int stride, int8_t* __restrict__ profb, int tr, int nblk,
-                           int* __restrict__ zero_a, int nza, int* __restrict__ zero_b, int nzb) {
+                           int* __restrict__ zero_a, int nza, int* __restrict__ zero_b, int nzb,
+                           uint8_t* __restrict__ zero_c = nullptr, int nzc = 0) {
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
   if (t0 < nza) zero_a[t0] = 0;
   if (t0 < nzb) zero_b[t0] = 0;
+  for (int t = t0; t < nzc; t += nt) zero_c[t] = 0;   // small databases: the flag bytes (no memset launch)
   const int total = kProfRows * stride;
   for (int t = t0; t < total; t += nt) {
     const int r = t / stride, i = t - r * stride;

@@ -79,6 +79,10 @@ __global__ void __launch_bounds__(kScanBlock) k_flag_compact_block(const uint8_t
                                                                    int* __restrict__ list, int* __restrict__ total,
                                                                    int* __restrict__ tail_groups) {
   __shared__ int warp_sums[kScanBlock / 32];
+  // programmatic dependent of the first pass (small databases): its flags are
+  // complete and visible after the wait; the rerun kernel behind may launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int S = (n + kScanBlock - 1) / kScanBlock;
   const int p0 = t * S, p1 = min(n, p0 + S);

@@ -848,6 +848,7 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
   __syncthreads();
   const int n_items = s_split;
   if (n_items <= 0) {
+    asm volatile("griddepcontrol.launch_dependents;");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
@@ -880,6 +881,10 @@ k_inter16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
     const uint32_t hmax = inter_group16<T, SMEM>(words + gd.base, gd.ncols, gprof, stride, m_pad, bnd, na2, nb2, lane);
     emit_pair(hmax, g, 2 * lane, gd.count, limit, pos_map, score_sorted, flag);
   }
+  // Out of work: a programmatic dependent launched behind this grid (the flag
+  // compaction of small databases) may become resident now; it waits for this
+  // grid's completion before reading anything.
+  asm volatile("griddepcontrol.launch_dependents;");
   // Launched as the programmatic dependent of k_intra16 (same stream): do not
   // retire before that grid has completed, so the stream's later work sees its
   // scores.  A no-op when there is no primary grid.
@@ -912,10 +917,15 @@ k_intra16(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
           uint2* __restrict__ scratch, long long scratch_cols, int* __restrict__ counter,
           int* __restrict__ score_sorted, uint8_t* __restrict__ flag, const int* __restrict__ len_sorted,
           const long long* __restrict__ ready_from, int mode) {
-  // mode bit 0: isolate the warps holding the longest pairs; bit 1: no chained stream
+  // mode bit 0: isolate the warps holding the longest pairs; bit 1: no chained stream;
+  // bit 2: no split of the critical pairs; bit 3: launched as the programmatic
+  // dependent of k_profiles (its CTAs become resident while the profiles are
+  // built and wait here for them, the counters and the flags)
   const bool isolate = mode & 1, chain_off = mode & 2, split_off = mode & 4;
+  if (mode & 8) asm volatile("griddepcontrol.wait;" ::: "memory");
   // The inter-task kernel may start beside this one (programmatic dependent
-  // launch): it only reads what was complete before this grid started.
+  // launch): it only reads what was complete before this grid started (with
+  // bit 3, after the wait above: k_profiles has then completed).
   asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ __align__(16) int8_t sprof[];
   __shared__ int s_split;

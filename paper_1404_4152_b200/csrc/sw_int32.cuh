@@ -165,6 +165,10 @@ k_list32(const uint2* __restrict__ words, const GroupDesc* __restrict__ groups,
          int alpha, int beta, uint2* __restrict__ scratch, long long scratch_cols,
          int* __restrict__ counter, int* __restrict__ score_sorted) {
   extern __shared__ __align__(16) int8_t sprof[];
+  // programmatic dependent of the flag compaction (small databases): the list
+  // and its count are visible after the wait; the ranking behind may launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const int n = list_count ? *list_count : n_list;
   if (n <= 0) return;
   const int8_t* prof = gprof;

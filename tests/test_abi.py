@@ -111,7 +111,7 @@ def _raw_create(L, **fields):
 
 @pytest.mark.parametrize("fields", [{"tuning.variant": 1}, {"tuning.tile_rows": 64}, {"tuning.threads": 512},
                                     {"tuning.intra_cols": 2}, {"tuning.pipe_chain": 12}, {"tuning.pipe_chain": 5},
-                                    {"tuning.intra_isolate": 2}, {"tuning.reserved": (ctypes.c_int32 * 1)(1)}, {"tuning.intra_chain": 1}, {"tuning.intra_split": 2},
+                                    {"tuning.intra_isolate": 2}, {"tuning.launch_chain": 1}, {"tuning.intra_chain": 1}, {"tuning.intra_split": 2},
                                     {"tuning.generic_gaps": 2},
                                     {"reserved": (ctypes.c_int32 * 4)(0, 1, 0, 0)},
                                     {"alloc": sw.ALLOC_FN(lambda n, c: None)}])

@@ -299,6 +299,27 @@ def test_int16_saturation_limits_exact():
         assert res.stats["n_rerun32"] == int((ref > limit).sum())
 
 
+def test_flags_reset_between_searches_on_one_handle():
+    """The int16 saturation flags are zeroed per search -- for small databases
+    inside k_profiles, with the intra-task pass launched as its programmatic
+    dependent: a saturating search, a clean one and the saturating one again on
+    one handle each re-align exactly the subjects above LIMIT16."""
+    M24 = blosum62()
+    limit = 32767 - 11
+    q_hot = _seq_with_self_score(40000, M24)
+    lens = np.concatenate([[q_hot.size, 50, q_hot.size], np.arange(1, 400, 7), [5000, 0]])
+    db = random_db(16, lens)
+    db.residues[db.offsets[0]:db.offsets[0] + q_hot.size] = q_hot
+    db.residues[db.offsets[2]:db.offsets[2] + q_hot.size] = q_hot[::-1]
+    q_cold = _query(700, seed=5)
+    with sw.Database(db.residues, db.offsets, db.lengths, device=0) as g:
+        for q in (q_hot, q_cold, q_hot, q_cold):
+            res = g.search(q, B62, 2, 12, k=5)
+            ref = oracle.db_scores(q, db, B62, 2, 12)
+            assert np.array_equal(res.scores, ref), q.size
+            assert res.stats["n_rerun32"] == int((ref > limit).sum()), q.size
+
+
 def test_s16_style_long_query_reruns():
     """8,000-residue query vs exact and near copies: self-scores ~42k exceed
     int16, forcing the int32 rerun (stress case S16)."""
