@@ -306,21 +306,23 @@ __global__ void __launch_bounds__(1024) k_rank_block(const int* __restrict__ sco
                                                      long long* __restrict__ out_ids, int* __restrict__ out_scores) {
   extern __shared__ unsigned long long skeys[];
   asm volatile("griddepcontrol.wait;" ::: "memory");   // programmatic dependent of the rerun (small databases)
-  // n <= kTopkSmemKeys = 12 x 1024: a thread's loads go out four items at a
-  // time before their first use (one memory latency per four items)
-  for (int p0 = threadIdx.x; p0 < n; p0 += 4 * 1024) {
-    int idx[4], sc[4];
+  // n <= kTopkSmemKeys = 12 x 1024: a thread's loads go out six items at a
+  // time before their first use (two rounds of two dependent memory latencies,
+  // perm then gid; twelve at a time spill under the 64-register cap)
+  constexpr int U = 6;
+  for (int p0 = threadIdx.x; p0 < n; p0 += U * 1024) {
+    int idx[U], sc[U];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < U; u++) {
       const int p = p0 + u * 1024;
       idx[u] = p < n ? perm[p] : 0;
       sc[u] = p < n ? score_sorted[p] : 0;
     }
-    unsigned long long id[4];
+    unsigned long long id[U];
 #pragma unroll
-    for (int u = 0; u < 4; u++) id[u] = gid ? (unsigned long long)gid[idx[u]] : (unsigned long long)idx[u];
+    for (int u = 0; u < U; u++) id[u] = gid ? (unsigned long long)gid[idx[u]] : (unsigned long long)idx[u];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < U; u++) {
       const int p = p0 + u * 1024;
       if (p < n) {
         if (scores_out) scores_out[idx[u]] = sc[u];
