@@ -160,6 +160,96 @@ __global__ void __launch_bounds__(NT, 1) k16(uint32_t* out, int ncols, int s16) 
   out[blockIdx.x * blockDim.x + threadIdx.x] = hmax ^ e;
 }
 
+
+// MODE 8 (round 2, third pass): PAIR profile of one R-row query tile in shared
+// memory, [625 = 25 x 25 residue pairs][SP words], word = (fsbt(q_i, b) << 16) |
+// (fsbt(q_i, a) & 0xffff): one LDS.128 per 4 rows per LANE (4 B per lane-row), no
+// merge instruction at all.  The first NPAIR rows of the tile use it, the other
+// R - NPAIR rows the int8 profile + PRMT (mode 0).  SP = NPAIR + 4 words keeps
+// 16-byte alignment and spreads the 625 rows over all eight 16-byte bank groups.
+// A production kernel would need every warp of the CTA on the SAME query tile
+// (tile-major schedule, table rebuilt per tile).
+template <int NPAIR, int R = 48, int NT = 384>
+__global__ void __launch_bounds__(NT, 1) kp(uint32_t* out, int ncols, int s8) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  constexpr int SP = NPAIR + 4;
+  int8_t* p8 = (int8_t*)sm;                                          // [25][s8] bytes
+  uint32_t* pp = (uint32_t*)(sm + ((25 * s8 + 15) / 16) * 16);       // [625][SP]
+  const int i0 = R * (blockIdx.x % (M / R));
+  for (int t = threadIdx.x; t < 25 * s8; t += blockDim.x) {
+    const int r = t / s8, i = t % s8;
+    p8[t] = r == 24 ? 0 : (int8_t)(((r * 7 + i * 13) % 15) - 4);
+  }
+  for (int t = threadIdx.x; t < 625 * SP; t += blockDim.x) {
+    const int pr = t / SP, i = t % SP + i0, ra = pr / 25, rb = pr % 25;
+    const int va = ra == 24 ? 0 : (((ra * 7 + i * 13) % 15) - 4), vb = rb == 24 ? 0 : (((rb * 7 + i * 13) % 15) - 4);
+    pp[t] = ((uint32_t)va & 0xffffu) | ((uint32_t)vb << 16);
+  }
+  __syncthreads();
+  uint32_t D[R], F[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) { D[r] = 0; F[r] = 0; }
+  uint32_t e = 0, hmax = 0, na2 = 0xfffefffeu, nb2 = 0xfff4fff4u;
+  uint32_t w = 0x9e3779b9u * (threadIdx.x + 1 + blockIdx.x * 977);
+  for (int j = 0; j < ncols; j++) {
+    w = w * 1664525u + 1013904223u;
+    const uint32_t rlo = ((w >> 24) * 25u) >> 8, rhi = (((w >> 16) & 255u) * 25u) >> 8;
+    const int8_t* a8 = p8 + rlo * s8 + i0;
+    const int8_t* b8 = p8 + rhi * s8 + i0;
+    const uint32_t* pq = pp + (rlo * 25u + rhi) * SP;
+    uint32_t hprev = e ^ (uint32_t)j, hodd = 0;
+    e = 0;
+#pragma unroll
+    for (int k8 = 0; k8 < R / 8; k8++) {
+      uint2 a, b;
+      uint4 q0, q1;
+      if (8 * k8 < NPAIR) { q0 = lds128(pq + 8 * k8); q1 = lds128(pq + 8 * k8 + 4); }
+      else {
+        a = *reinterpret_cast<const uint2*>(a8 + 8 * k8);
+        b = *reinterpret_cast<const uint2*>(b8 + 8 * k8);
+      }
+#pragma unroll
+      for (int rr = 0; rr < 8; rr++) {
+        const int r = 8 * k8 + rr;
+        const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);
+        uint32_t sn;
+        if (8 * k8 < NPAIR) {
+          const uint4& q = rr < 4 ? q0 : q1;
+          sn = (rr & 3) == 0 ? q.x : (rr & 3) == 1 ? q.y : (rr & 3) == 2 ? q.z : q.w;
+        } else {
+          sn = prmt(rr < 4 ? a.x : a.y, rr < 4 ? b.x : b.y, sel_pair(rr & 3));
+        }
+        D[r] = __vadd2(hprev, sn);
+        const uint32_t hb = __vadd2(h, nb2);
+        e = __viaddmax_s16x2_relu(e, na2, hb);
+        F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+        if (rr & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
+        else hodd = h;
+        hprev = h;
+      }
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = hmax ^ e;
+}
+
+template <int NPAIR, int R = 48, int NT = 384>
+void runp(const char* name, uint32_t* d_out, int nsm) {
+  const int ncols = 4096, threads = NT;
+  const int s8 = M + 8;
+  const size_t smem = ((25 * s8 + 15) / 16) * 16 + 625 * (size_t)(NPAIR + 4) * 4;
+  cudaFuncSetAttribute(kp<NPAIR, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; rep++) {
+    cudaEventRecord(e0); kp<NPAIR, R, NT><<<nsm, threads, smem>>>(d_out, ncols, s8); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); float ms; cudaEventElapsedTime(&ms, e0, e1); if (rep && ms < best) best = ms;
+  }
+  cudaError_t err = cudaGetLastError();
+  const double cells = 2.0 * R * ncols * threads * (double)nsm;
+  printf("%-34s R=%d NT=%d pair rows %d of %d, smem %zu B  %.1f Gcell/s %s\n", name, R, NT, NPAIR, R, smem,
+         cells / (best * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
+}
+
 template <int MODE, int LW, int R = 48, int NT = 384>
 void run16(const char* name, uint32_t* d_out, int nsm, int s16) {
   const int ncols = 4096, threads = NT;
@@ -195,6 +285,21 @@ void run(const char* name, uint32_t* d_out, int nsm, int s32) {
 int main() {
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   uint32_t* d_out; cudaMalloc(&d_out, 4 * nsm * 512);
+  if (getenv("PAIR")) {
+    run<0>("mode0 int8+PRMT", d_out, nsm, M + 2);
+    runp<0>("mode8 pair profile", d_out, nsm);
+    runp<8>("mode8 pair profile", d_out, nsm);
+    runp<16>("mode8 pair profile", d_out, nsm);
+    runp<24>("mode8 pair profile", d_out, nsm);
+    runp<32>("mode8 pair profile", d_out, nsm);
+    runp<40>("mode8 pair profile", d_out, nsm);
+    runp<48>("mode8 pair profile", d_out, nsm);
+    runp<32, 32, 512>("mode8 pair profile", d_out, nsm);
+    runp<16, 32, 512>("mode8 pair profile", d_out, nsm);
+    runp<40, 40, 384>("mode8 pair profile", d_out, nsm);
+    runp<64, 64, 256>("mode8 pair profile", d_out, nsm);
+    return 0;
+  }
   if (getenv("INT16")) {
     run<0>("mode0 int8+PRMT", d_out, nsm, M + 2);
     for (int s16 : {M + 8, M + 16, M + 32, M + 64}) {
