@@ -11,18 +11,20 @@ namespace swk {
 // substitution pair is a single word of the pair profile
 //   prof2[r][i] = (fsbt(qa_i, r), fsbt(qb_i, r))   (int16x2)
 // and the PRMT of the single-query kernel disappears (3.5 alu ops per row).
-// The row stride is odd in words, so 32 lanes reading rows of different
-// residues hit different banks (LDS.32, conflict-free).
+// The row stride is 2 mod 32 words (odd in 8-byte units) and tiles start at even
+// rows, so two rows come in one LDS.64 and only residues r, r + 16 share banks.
 // ---------------------------------------------------------------------------
 template <int R>
 __device__ __forceinline__ uint32_t colq(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t& e, uint32_t htop,
                                          const uint32_t* __restrict__ p, uint32_t na2, uint32_t nb2,
                                          uint32_t& hmax) {
   uint32_t hprev = htop, hodd = 0u;
+  uint2 pw = make_uint2(0u, 0u);
 #pragma unroll
   for (int r = 0; r < R; r++) {
     const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);
-    D[r] = __vadd2(hprev, p[r]);                               // H(i-1,j) + (fsbt(qa_i,s_{j+1}), fsbt(qb_i,s_{j+1}))
+    if (!(r & 1)) pw = *reinterpret_cast<const uint2*>(p + r);  // rows r, r+1 in one LDS.64 (p is 8-byte aligned)
+    D[r] = __vadd2(hprev, (r & 1) ? pw.y : pw.x);              // H(i-1,j) + (fsbt(qa_i,s_{j+1}), fsbt(qb_i,s_{j+1}))
     const uint32_t hb = __vadd2(h, nb2);
     e = __viaddmax_s16x2_relu(e, na2, hb);
     F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
