@@ -250,6 +250,69 @@ void runp(const char* name, uint32_t* d_out, int nsm) {
          cells / (best * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
 }
 
+
+// MODE 9: mode 0 (int8 profile + PRMT) with ONE LDS.128 per 16 rows per subject
+// instead of LDS.64 per 8 rows (row stride 16 * odd bytes).
+template <int R = 48, int NT = 384>
+__global__ void __launch_bounds__(NT, 1) k9(uint32_t* out, int ncols, int s8) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  int8_t* p8 = (int8_t*)sm;
+  for (int t = threadIdx.x; t < 25 * s8; t += blockDim.x) {
+    const int r = t / s8, i = t % s8;
+    p8[t] = r == 24 ? 0 : (int8_t)(((r * 7 + i * 13) % 15) - 4);
+  }
+  __syncthreads();
+  uint32_t D[R], F[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) { D[r] = 0; F[r] = 0; }
+  uint32_t e = 0, hmax = 0, na2 = 0xfffefffeu, nb2 = 0xfff4fff4u;
+  uint32_t w = 0x9e3779b9u * (threadIdx.x + 1 + blockIdx.x * 977);
+  const int i0 = R * (blockIdx.x % (M / R));
+  for (int j = 0; j < ncols; j++) {
+    w = w * 1664525u + 1013904223u;
+    const uint32_t rlo = ((w >> 24) * 25u) >> 8, rhi = (((w >> 16) & 255u) * 25u) >> 8;
+    const int8_t* a8 = p8 + rlo * s8 + i0;
+    const int8_t* b8 = p8 + rhi * s8 + i0;
+    uint32_t hprev = e ^ (uint32_t)j, hodd = 0;
+    e = 0;
+#pragma unroll
+    for (int k16 = 0; k16 < R / 16; k16++) {
+      const uint4 a = lds128(a8 + 16 * k16), b = lds128(b8 + 16 * k16);
+      const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int rr = 0; rr < 16; rr++) {
+        const int r = 16 * k16 + rr;
+        const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);
+        const uint32_t sn = prmt(aw[rr >> 2], bw[rr >> 2], sel_pair(rr & 3));
+        D[r] = __vadd2(hprev, sn);
+        const uint32_t hb = __vadd2(h, nb2);
+        e = __viaddmax_s16x2_relu(e, na2, hb);
+        F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+        if (rr & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
+        else hodd = h;
+        hprev = h;
+      }
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = hmax ^ e;
+}
+template <int R = 48, int NT = 384>
+void run9(uint32_t* d_out, int nsm, int s8) {
+  const int ncols = 4096, threads = NT;
+  const size_t smem = 25 * (size_t)s8;
+  cudaFuncSetAttribute(k9<R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; rep++) {
+    cudaEventRecord(e0); k9<R, NT><<<nsm, threads, smem>>>(d_out, ncols, s8); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); float ms; cudaEventElapsedTime(&ms, e0, e1); if (rep && ms < best) best = ms;
+  }
+  cudaError_t err = cudaGetLastError();
+  const double cells = 2.0 * R * ncols * threads * (double)nsm;
+  printf("mode9 int8+PRMT, LDS.128 per 16 rows  R=%d NT=%d s8=%d  %.1f Gcell/s %s\n", R, NT, s8,
+         cells / (best * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
+}
+
 template <int MODE, int LW, int R = 48, int NT = 384>
 void run16(const char* name, uint32_t* d_out, int nsm, int s16) {
   const int ncols = 4096, threads = NT;
@@ -298,6 +361,13 @@ int main() {
     runp<16, 32, 512>("mode8 pair profile", d_out, nsm);
     runp<40, 40, 384>("mode8 pair profile", d_out, nsm);
     runp<64, 64, 256>("mode8 pair profile", d_out, nsm);
+    return 0;
+  }
+  if (getenv("LDS128")) {
+    run<0>("mode0 int8+PRMT", d_out, nsm, M + 2);
+    for (int s8 : {496, 528, 560, 592, 624}) run9<48, 384>(d_out, nsm, s8);
+    run9<32, 512>(d_out, nsm, 496);
+    run9<64, 256>(d_out, nsm, 496);
     return 0;
   }
   if (getenv("INT16")) {
