@@ -392,6 +392,11 @@ int main() {
     run<0, 0, 96, 320>("mode0", d_out, nsm, M + 2);
     run<0, 0, 64, 320>("mode0", d_out, nsm, M + 2);
     run<0, 0, 40, 384>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 40, 448>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 40, 416>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 32, 576>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 32, 544>("mode0", d_out, nsm, M + 2);
+    run<0, 0, 48, 416>("mode0", d_out, nsm, M + 2);
     return 0;
   }
   for (int s32 : {M + 2, M + 4, M + 1 + 1 + 32}) {
