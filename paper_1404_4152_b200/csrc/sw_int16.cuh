@@ -18,11 +18,42 @@ namespace swk {
 // alu-pipe VIADDMNMX, and D is updated in place (no register moves).  (Taking
 // E - alpha off the E chain costs a third VIADD.16x2 and measured 3% slower.)
 // ---------------------------------------------------------------------------
-template <int R>
+template <int R, bool A16 = false>
 __device__ __forceinline__ uint32_t col16(uint32_t (&D)[R], uint32_t (&F)[R], uint32_t& e, uint32_t htop,
                                           const int8_t* __restrict__ plo, const int8_t* __restrict__ phi,
                                           uint32_t na2, uint32_t nb2, uint32_t& hmax) {
   uint32_t hprev = htop, hodd = 0u;
+  if constexpr (A16 && R % 16 == 0) {
+    // One LDS.128 per 16 rows per subject (the profile row stride and every full
+    // tile's first row are multiples of 16 bytes): half the profile loads.
+    uint4 a = *reinterpret_cast<const uint4*>(plo);
+    uint4 b = *reinterpret_cast<const uint4*>(phi);
+#pragma unroll
+    for (int k = 0; k < R / 16; k++) {
+      uint4 an = a, bn = b;
+      if (k + 1 < R / 16) {
+        an = *reinterpret_cast<const uint4*>(plo + 16 * (k + 1));
+        bn = *reinterpret_cast<const uint4*>(phi + 16 * (k + 1));
+      }
+      const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int rr = 0; rr < 16; rr++) {
+        const int r = 16 * k + rr;
+        const uint32_t h = __vimax3_s16x2(D[r], e, F[r]);
+        const uint32_t sn = prmt(aw[rr >> 2], bw[rr >> 2], sel_pair(rr & 3));
+        D[r] = __vadd2(hprev, sn);
+        const uint32_t hb = __vadd2(h, nb2);
+        e = __viaddmax_s16x2_relu(e, na2, hb);
+        F[r] = __viaddmax_s16x2_relu(F[r], na2, hb);
+        if (rr & 1) hmax = __vimax3_s16x2(hmax, hodd, h);
+        else hodd = h;
+        hprev = h;
+      }
+      a = an;
+      b = bn;
+    }
+    return hprev;
+  }
   uint2 a = *reinterpret_cast<const uint2*>(plo);
   uint2 b = *reinterpret_cast<const uint2*>(phi);
 #pragma unroll
@@ -146,7 +177,7 @@ __device__ __forceinline__ void col16x2(uint32_t (&D)[R], uint32_t (&F)[R],
 
 // Packed residue pair (lo, hi codes) of column c of this lane: word c/6, field c%6.
 
-template <int R>
+template <int R, bool A16 = (R % 16 == 0)>   // A16: this tile's first profile row is 16-byte aligned
 __device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
                                        const int8_t* __restrict__ prof, int stride, int i0,
                                        uint2* __restrict__ bnd, bool first, bool last,
@@ -161,7 +192,7 @@ __device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
   {  // virtual column j = -1 (all-zero boundary): primes D[r] = fsbt(q_{i0+r}, s_0)
     const uint2 w0 = lw[0];
     uint32_t e0 = 0u;
-    col16<R>(D, F, e0, 0u, pr + (w0.x & 31u) * stride, pr + (w0.y & 31u) * stride, na2, nb2, hmax);
+    col16<R, A16>(D, F, e0, 0u, pr + (w0.x & 31u) * stride, pr + (w0.y & 31u) * stride, na2, nb2, hmax);
   }
   // Columns are taken two at a time (A = j, B = j+1).  The residue words of the
   // next pair's "next columns" (j+3, j+4) and its boundary rows (j+2, j+3) are
@@ -185,9 +216,9 @@ __device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
                eB, tB, pr + ((wB.x >> shB) & 31u) * stride, pr + ((wB.y >> shB) & 31u) * stride,
                na2, nb2, hmax, hlA, hlB);
 #else
-    hlA = col16<R>(D, F, eA, tA, pr + ((wA.x >> shA) & 31u) * stride, pr + ((wA.y >> shA) & 31u) * stride,
+    hlA = col16<R, A16>(D, F, eA, tA, pr + ((wA.x >> shA) & 31u) * stride, pr + ((wA.y >> shA) & 31u) * stride,
                    na2, nb2, hmax);
-    hlB = col16<R>(D, F, eB, tB, pr + ((wB.x >> shB) & 31u) * stride, pr + ((wB.y >> shB) & 31u) * stride,
+    hlB = col16<R, A16>(D, F, eB, tB, pr + ((wB.x >> shB) & 31u) * stride, pr + ((wB.y >> shB) & 31u) * stride,
                    na2, nb2, hmax);
 #endif
     wA = res_word(lw, j + 3, nwords);
@@ -200,7 +231,7 @@ __device__ __forceinline__ void tile16(const uint2* __restrict__ gw, int ncols,
   if (j < ncols) {                                 // odd tail column
     const int shA = res_shift(j + 1);
     uint32_t e = bE.x;
-    const uint32_t hl = col16<R>(D, F, e, bE.y, pr + ((wA.x >> shA) & 31u) * stride,
+    const uint32_t hl = col16<R, A16>(D, F, e, bE.y, pr + ((wA.x >> shA) & 31u) * stride,
                                  pr + ((wA.y >> shA) & 31u) * stride, na2, nb2, hmax);
     if (!last) bnd[j * 32 + lane] = make_uint2(e, hl);
   }
@@ -211,7 +242,7 @@ __device__ __forceinline__ void tile16_rem(int rem, const uint2* gw, int ncols, 
                                            int stride, int i0, uint2* bnd, bool first,
                                            uint32_t na2, uint32_t nb2, uint32_t& hmax, int lane) {
   if constexpr (R >= 8) {
-    if (rem == R) tile16<R>(gw, ncols, prof, stride, i0, bnd, first, true, na2, nb2, hmax, lane);
+    if (rem == R) tile16<R, (T % 16 == 0) && (R % 16 == 0)>(gw, ncols, prof, stride, i0, bnd, first, true, na2, nb2, hmax, lane);
     else tile16_rem<T, R - 8>(rem, gw, ncols, prof, stride, i0, bnd, first, na2, nb2, hmax, lane);
   }
 }
